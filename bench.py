@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the FP8-LM data-parallel hot path on B200.
+
+One "step" = one pass of the whole hot path over one
+synthetic gradient set already resident in HBM:
+  amax_scale_sync (A1 amax, A2 mu/scale/MIN) -> fp8_grad_allreduce (A3 quantize,
+  A4/A5 reduce-scatter + FP32 reduce + all-gather, Eq. 6 scale, mu update) ->
+  fp8_adam_step (A6 dequant + A7 two-pass JIT FP8 AdamW, FP8 weight copy).
+
+Default workload: BASELINE.json configs[1], "GPT-125M full gradient set (per-layer
+tensors) on 1 B200" (147 tensors, 123.69M params).  --config gpt-7b selects configs[2].
+N > 1 (torchrun): one rank per GPU, NCCL over NVLink, each rank holding its own full
+gradient set (data parallelism: per-GPU work fixed -> "scaling": "weak").
+
+metric (BASELINE.json): GB/s of algorithmic bytes moved per step, whole job (sum over
+ranks) = N * bytes_per_rank / max-over-ranks step time, where bytes_per_rank = params
+x (27 B at N = 1; 28 + 1/N + 2(N-1)/N B at N >= 2) — SURVEY §8(d).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP8 grad reduce+Adam step: GB/s & % HBM/NVLink roofline at 1/2/4/8 B200"
+UNIT = "GB/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="gpt-125m", choices=["gpt-125m", "gpt-7b", "gpt-13b"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"], help="gradient dtype")
+    ap.add_argument("--lr", type=float, default=6e-4)   # GPT-125M max LR, Table 1
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def alg_bytes_per_param(N: int) -> float:
+    """A1 4 + A3 5 + A7 18 at N = 1 (A4/A5 identity); at N >= 2 add the
+    reduce (1 + 1/N) and the all-gather write 2(N-1)/N."""
+    if N == 1:
+        return 27.0
+    return 28.0 + 1.0 / N + 2.0 * (N - 1) / N
+
+
+# per-launch algorithmic bytes per parameter of each kernel (LOCAL / NCCL modes)
+KERNEL_BYTES = {
+    "amax": 4.0, "quantize": 5.0, "adam_pass1": 6.0, "adam_pass2": 12.0,
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                index = int(vis.split(",")[index])
+            except (ValueError, IndexError):
+                pass
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-i", str(index), "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(parts[1]), smax=float(parts[2]), hw=parts[5], hwt=parts[6],
+                                 swt=parts[7], pcap=parts[8]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        reasons = set()
+        for r in rows:
+            for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
+                            ("swt", "sw_thermal_slowdown"), ("pcap", "sw_power_cap")):
+                if r[k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r["sm"] for r in rows), "sm_max_mhz": max(r["smax"] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ oracle (CPU) legs
+def oracle_sample(specs, config):
+    """Bounded sample of the workload for the CPU oracle: the tensors of the first
+    layer(s) (~10-20 s of single-core oracle work for GPT-125M)."""
+    want = ("layer0.", "layer1.") if config == "gpt-125m" else ("layer0.ln", "layer0.qkv", "layer0.proj")
+    return [t for t, s in enumerate(specs) if s.name.startswith(want)]
+
+
+def run_oracle_step(specs, idx, rank, step, states):
+    import numpy as np
+    import torch
+    import synth
+    from oracle import adam as OA
+    from oracle import step as OS
+    grads = []
+    for t in idx:
+        g = torch.empty(specs[t].numel, dtype=torch.float32)
+        synth.fill_gradient(g, 1, t, rank)
+        grads.append(g.numpy())
+    t0 = time.perf_counter()
+    res = OS.train_step([grads], [np.float32(1.0)] * len(idx), states, OA.hyper_params(6e-4, step))
+    return time.perf_counter() - t0, res["states"]
+
+
+def oracle_states(specs, idx):
+    import torch
+    import synth
+    from oracle import adam as OA
+    out = []
+    for t in idx:
+        w = torch.empty(specs[t].numel, dtype=torch.float32)
+        synth.fill_weights(w, t)
+        out.append(OA.init_state(w.numpy()))
+    return out
+
+
+def cpu_baseline(specs, config):
+    idx = oracle_sample(specs, config)
+    params = sum(specs[t].numel for t in idx)
+    states = oracle_states(specs, idx)
+    dt, _ = run_oracle_step(specs, idx, 0, 1, states)
+    gbs = alg_bytes_per_param(1) * params / dt / 1e9
+    return {"value": gbs, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{len(idx)} tensors ({params} params: {specs[idx[0]].name}..{specs[idx[-1]].name}) "
+                      f"of {config}, one full step, N=1, numpy single-thread; {dt:.2f} s",
+            "host_cores_available": len(os.sched_getaffinity(0))}
+
+
+def run_reference(args, specs, world, rank):
+    """--impl reference: the CPU oracle as the reference arm, same metric/config/unit."""
+    if rank != 0:
+        return
+    idx = oracle_sample(specs, args.config)
+    params = sum(specs[t].numel for t in idx)
+    states = oracle_states(specs, idx)
+    step = 0
+    for _ in range(args.warmup):
+        step += 1
+        _, states = run_oracle_step(specs, idx, 0, step, states)
+    tot = 0.0
+    for _ in range(args.steps):
+        step += 1
+        dt, states = run_oracle_step(specs, idx, 0, step, states)
+        tot += dt
+    ms = tot / args.steps * 1e3
+    value = alg_bytes_per_param(1) * params / (ms / 1e3) / 1e9
+    sample = (f"{len(idx)} tensors ({params} params) of {args.config} per step, N=1 math, "
+              f"numpy single-thread")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config} gradient set, oracle sample", "tensors": len(idx),
+                       "params": params},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    import synth
+    cfg_layers = None
+    specs = synth.gpt_gradient_set(args.config, cfg_layers)
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, specs, world, rank)
+        return
+
+    import torch
+    world, rank, local = dist_setup(args)
+    import paper_2310_18313_b200 as B
+
+    numels = [s.numel for s in specs]
+    params = sum(numels)
+    N = world
+    comm = B.Comm.from_torch_distributed() if N > 1 else None
+    mode = B.MODE_NCCL if N > 1 else B.MODE_LOCAL
+    plan = B.Plan(numels, mode=mode, nranks=N, rank=rank)
+    gdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    w0 = plan.flat(torch.float32)
+    for t, v in enumerate(plan.views(w0)):
+        synth.fill_weights(v, t)
+    grads = plan.flat(gdt)
+    for t, v in enumerate(plan.views(grads)):
+        synth.fill_gradient(v, 1, t, rank)
+    dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr)
+    del w0
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        dp.step(grads)
+    torch.cuda.synchronize()
+
+    # clock sampler runs through a ~1 s untimed soak and the timed region
+    sampler = ClockSampler(local)
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 1.0:
+        dp.step(grads)
+        torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps, per-launch CUDA events on the launch stream
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    B.prof_enable(True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        dp.step(grads)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    B.prof_enable(False)
+    prof = B.prof_read()
+    clocks = sampler.stop()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms_local, world)
+
+    bytes_rank = alg_bytes_per_param(N) * params * (1.0 if args.dtype == "f32" else 1.0)
+    if args.dtype == "bf16":
+        bytes_rank -= 2.0 * 2 * params      # A1 and A3 read 2 B instead of 4
+    value = N * bytes_rank / (ms / 1e3) / 1e9
+
+    # ---------------- roofline of the dominant kernel (ours, largest device time)
+    hbm, hbm_kind = peaks()
+    ours = {k: v for k, v in prof.items() if v["ours"]}
+    dom = max(ours, key=lambda k: ours[k]["ms"]) if ours else None
+    roof = None
+    if dom:
+        per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
+        bpp = KERNEL_BYTES.get(dom)
+        if bpp is not None:
+            if args.dtype == "bf16" and dom in ("amax", "quantize"):
+                bpp -= 2.0
+            achieved = bpp * params / (per_launch_ms / 1e3) / 1e9
+            roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "peak_kind": hbm_kind, "traffic": None,
+                    "alg_bytes_per_launch": bpp * params, "avg_launch_ms": per_launch_ms,
+                    "share_of_step": ours[dom]["ms"] / (ms_local * args.steps)}
+    launches = int(sum(v["launches"] for v in ours.values()) / args.steps)
+    breakdown = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
+                 for k, v in prof.items()}
+
+    # ---------------- e2e: host gradients (pinned) -> device, step, results -> host
+    e2e = None
+    if not args.no_e2e:
+        host_g = torch.empty(grads.numel(), dtype=gdt, pin_memory=True)
+        host_g.copy_(grads)
+        out_h = torch.empty(3 * plan.T + 1, dtype=torch.float32, pin_memory=True)
+        out_d = torch.empty(3 * plan.T + 1, dtype=torch.float32, device="cuda")
+        def e2e_step():
+            grads.copy_(host_g, non_blocking=True)
+            dp.step(grads)
+            torch.cat([dp.mu, dp.s_g, dp.sat.float(), dp.skip.float()], out=out_d)
+            out_h.copy_(out_d, non_blocking=True)
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ems = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        e2e = {"value": N * bytes_rank / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": host_g.numel() * host_g.element_size(),
+               "d2h_bytes_per_step": out_h.numel() * 4}
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(specs, args.config)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"{args.config} full gradient set (BASELINE.json configs["
+                                   f"{ {'gpt-125m': 1, 'gpt-7b': 2, 'gpt-13b': 3}[args.config] }])",
+                       "tensors": plan.T, "params": params, "grad_dtype": args.dtype,
+                       "alg_bytes_per_param_per_rank": bytes_rank / params,
+                       "parallelism": f"dp{N}" if N > 1 else "single", "state_scaling": "jit",
+                       "l2": "inputs larger than L2 (step moves %.2f GB/rank > 126 MB)" % (bytes_rank / 1e9),
+                       "hbm_frac_of_8tbs": value / N / 8000.0},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks, "kernels": breakdown,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        import torch.distributed as dist
+        dist.barrier()
+        comm.close()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,226 @@
+/*
+ * fp8lm.h — C ABI of the FP8-LM data-parallel hot path on B200 (sm_100a).
+ *
+ * FP8-LM (arXiv 2310.18313), PAPER.md:
+ *   §2.1 "FP8 Gradient and All-Reduce Communication"  P:95-142  (Eq. 3-6)
+ *   §2.2 "FP8 Optimizer"                              P:146-179 (Eq. 7-8)
+ *   §2.3 FP8 ZeRO, Alg. 1
+ *   App. A FP8 formats, Table 5
+ *   App. B JIT / delayed tensor scaling
+ * Readings of ambiguous passages are numbered R1..R24 in DESIGN.md §3.
+ *
+ * CONVENTIONS (apply to every call)
+ *   - Pointers are DEVICE pointers unless the parameter says "host".
+ *   - The caller owns all memory (PyTorch allocates it).  The library allocates
+ *     nothing on the hot path; it owns only plan / communicator objects.
+ *   - Every device-side call is asynchronous on `stream` (a cudaStream_t; NULL =
+ *     legacy default stream) and performs no host synchronisation.
+ *   - Return value: FP8LM_OK (0) or a negative fp8lm_status.  Argument errors are
+ *     detected on the host and returned before anything is enqueued.  CUDA / NCCL
+ *     launch errors return FP8LM_ECUDA / FP8LM_ENCCL.  fp8lm_last_error() gives a
+ *     thread-local message.  Nothing throws across the ABI.
+ *   - A non-finite gradient is NOT an error: it sets the device flag *skip = 1,
+ *     the optimizer step becomes a no-op and mu halves (R14).
+ *
+ * FLAT LAYOUT ("plan")
+ *   A plan describes T tensors (numel[t]) packed into flat buffers, tensor t at
+ *   element offset fp8lm_plan_offset(t) (a multiple of FP8LM_ALIGN_ELEMS).  The
+ *   gradient buffer (fp32 or bf16), the E4M3 gradient codes and every optimizer
+ *   state buffer use the same element offsets (DDP-bucket style: autograd writes
+ *   into views of the flat gradient buffer).  Per-tensor scalars are arrays [T].
+ *
+ * SCALING TENSORS ("(g'_i, s'_i) ... The actual weight gradient is g'_i/s'_i")
+ *   logical value = decode(code) * scale_inv, with scale_inv = fl(1/scale)  (R8).
+ */
+#ifndef FP8LM_H
+#define FP8LM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FP8LM_ABI_VERSION 1
+#define FP8LM_ALIGN_ELEMS 64      /* tensor offsets in flat buffers are multiples of this */
+#define FP8LM_MAX_SIM_RANKS 16    /* simulated ranks on one device (config C1) */
+
+typedef enum {
+  FP8LM_OK = 0,
+  FP8LM_EINVAL = -1,        /* bad argument (host-side check)               */
+  FP8LM_ECUDA = -2,         /* CUDA runtime / launch error                   */
+  FP8LM_ENCCL = -3,         /* NCCL error                                    */
+  FP8LM_EWORKSPACE = -4,    /* workspace missing / too small / plan unbound  */
+  FP8LM_EUNSUPPORTED = -5   /* built without NCCL, or unsupported dtype     */
+} fp8lm_status;
+
+typedef enum {
+  FP8LM_E4M3 = 0,   /* App. A: S1E4M3, bias 7, max 448, NaN = S.1111.111, no inf  */
+  FP8LM_E5M2 = 1,   /* App. A: S1E5M2, bias 15, max 57344, inf, NaN              */
+  FP8LM_F16 = 2,
+  FP8LM_BF16 = 3,
+  FP8LM_F32 = 4
+} fp8lm_dtype;
+
+typedef enum {
+  FP8LM_MODE_LOCAL = 0,      /* nranks must be 1: one process, one GPU, no exchange     */
+  FP8LM_MODE_SIMULATED = 1,  /* nranks simulated ranks whose gradients all live on this
+                                device (config C1); the exchange is a local read       */
+  FP8LM_MODE_NCCL = 2        /* one process per GPU; exchange over NCCL (NVLink)       */
+} fp8lm_mode;
+
+typedef struct fp8lm_plan fp8lm_plan;   /* opaque */
+typedef struct fp8lm_comm fp8lm_comm;   /* opaque: owns an ncclComm_t */
+
+/* A set of T scaling tensors in one flat buffer (D1/D4 of SURVEY §2.2).
+ * data: flat codes (uint8 for E4M3, uint16 for FP16) at the plan's offsets.
+ * scale / scale_inv / amax: device float[T]. */
+typedef struct {
+  void* data;
+  float* scale;
+  float* scale_inv;
+  float* amax;
+} fp8lm_stensors;
+
+/* AdamW scalars for one step (P:301 beta1 = 0.9, beta2 = 0.95, weight decay 0.1;
+ * eps, bias correction R15).  Each field is computed on the host in double and
+ * rounded once to float (R24) — see fp8lm_adam_hp_make. */
+typedef struct {
+  float beta1, beta2;
+  float one_minus_beta1, one_minus_beta2;
+  float eps;
+  float decay;          /* fl(1 - lr * weight_decay)            */
+  float step_size;      /* fl(lr / (1 - beta1^step))             */
+  float inv_bc2_sqrt;   /* fl(1 / sqrt(1 - beta2^step))          */
+} fp8lm_adam_hp;
+
+/* ------------------------------------------------------------------ misc (host) */
+int fp8lm_version(void);                       /* FP8LM_ABI_VERSION */
+const char* fp8lm_last_error(void);            /* thread-local message of the last failure */
+int fp8lm_has_nccl(void);                      /* 1 if built with NCCL */
+
+/* Host: fill *out (host) from the hyper-parameters; step >= 1.  EINVAL on step < 1 or
+ * non-finite inputs. */
+int fp8lm_adam_hp_make(double lr, double beta1, double beta2, double eps,
+                       double weight_decay, int64_t step, fp8lm_adam_hp* out);
+
+/* Host: Alg. 1 "Greedy Distribution Algorithm for ZeRO".  numels [T]
+ * (host) are the tensor sizes c_i; owner_out [T] (host) receives the GPU of each
+ * tensor; load_out [nranks] (host) the loads u_j.  Ties: stable sort by ascending
+ * index, argmin by lowest device (R21).  EINVAL if nranks < 1 or T < 0. */
+int fp8lm_zero_plan(int32_t T, const int64_t* numels, int32_t nranks,
+                    int32_t* owner_out, int64_t* load_out);
+
+/* ------------------------------------------------------------- communicator (NCCL) */
+/* Host: ncclGetUniqueId into id_out[128] (host).  Rank 0 calls it and broadcasts the
+ * bytes with torch.distributed (plumbing). */
+int fp8lm_comm_unique_id(uint8_t* id_out);
+/* Host: ncclCommInitRank on the CURRENT CUDA device.  *out receives the handle. */
+int fp8lm_comm_init(int32_t nranks, int32_t rank, const uint8_t* id, fp8lm_comm** out);
+int fp8lm_comm_destroy(fp8lm_comm* comm);
+
+/* --------------------------------------------------------------------- the plan */
+/* Host: build the flat layout, chunk tables and (mode NCCL) the reduce-scatter shard
+ * map for T tensors.  numels (host) [T], each >= 0.  nranks >= 1; rank in [0,nranks)
+ * (ignored unless mode == NCCL).  EINVAL on bad arguments. */
+int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nranks,
+                      int32_t rank, fp8lm_plan** out);
+int fp8lm_plan_destroy(fp8lm_plan* plan);
+int64_t fp8lm_plan_offset(const fp8lm_plan* plan, int32_t t);  /* element offset of tensor t, -1 if bad */
+int64_t fp8lm_plan_total(const fp8lm_plan* plan);              /* elements of every flat buffer */
+int64_t fp8lm_plan_g8_bytes(const fp8lm_plan* plan);           /* bytes of the reduced-code buffer g8
+                                                                  (>= total; N*S in mode NCCL) */
+int64_t fp8lm_plan_shard_bytes(const fp8lm_plan* plan);        /* S: bytes each rank reduces (NCCL) */
+int64_t fp8lm_plan_shard_begin(const fp8lm_plan* plan, int32_t rank); /* = rank * S */
+size_t fp8lm_plan_workspace_bytes(const fp8lm_plan* plan);
+/* Upload the plan's tables into the caller-owned device workspace `ws` (>=
+ * fp8lm_plan_workspace_bytes, 256-byte aligned) and zero its accumulators on
+ * `stream`; synchronises `stream` before returning (one-time setup, host tables are
+ * pageable).  Must precede every call below that takes the plan.
+ * EWORKSPACE if ws is NULL / too small / misaligned. */
+int fp8lm_plan_bind(fp8lm_plan* plan, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------- (1) fp8_quantize: one scaling tensor */
+/* App. B JIT scaling + App. A encode.  src: n elements of src_dtype (F32 or BF16),
+ * any alignment.  fmt: E4M3 or E5M2 (codes to dst, uint8[n]) or F16 (uint16[n]).
+ * jit = 1: amax = max|src| -> *amax, scale = fl(fmt_max / amax) (1 if amax is 0 or
+ *          the ratio overflows) -> *scale, *scale_inv = fl(1/scale), then encode.
+ * jit = 0: use the scale already in *scale (amax not written).
+ * Encode: code = satRNE(fl(src * scale)) (R11: saturating round-to-nearest-even).
+ * sat_count (nullable): += number of codes whose magnitude is the format max. */
+int fp8lm_quantize(const void* src, int32_t src_dtype, int64_t n, int32_t fmt, void* dst,
+                   float* scale, float* scale_inv, float* amax, int32_t jit,
+                   uint32_t* sat_count, void* stream);
+/* dst[i] = fl(decode(codes[i]) * (*scale_inv)), fp32 output. */
+int fp8lm_dequantize(const void* codes, int32_t fmt, int64_t n, const float* scale_inv,
+                     float* dst, void* stream);
+
+/* ---------------------------- (2) amax_scale_sync: Eq. 3-4, A1 + A2 */
+/* grads: flat gradient buffer (src_dtype F32 or BF16) in plan layout.  In mode
+ * SIMULATED, grads is a HOST array of nranks device pointers (one flat buffer per
+ * simulated rank) cast to const void*; otherwise it is the device pointer itself.
+ *   amax_r[t] = max_i |g_r[t][i]|                 -> amax_out [T] (SIMULATED: [nranks*T],
+ *                                                   rank-major); NaN/inf propagate (R14)
+ *   s_r[t]    = fl(fl(448 / amax_r[t]) * mu[t])   (0 if non-finite, +inf if amax == 0)
+ *   s_g[t]    = min_r s_r[t]  (Eq. 4; NCCL: ncclAllReduce MIN over `comm`)
+ *   s_g == 0 -> *skip = 1;  s_g == +inf -> s_g = 1.         -> s_g [T], skip [1]
+ * mu [T] is read only.  comm must be non-NULL iff mode == NCCL. */
+int fp8lm_amax_scale_sync(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
+                          int32_t src_dtype, const float* mu, float* amax_out,
+                          float* s_g, int32_t* skip, void* stream);
+
+/* ----------------------------- (3) fp8_grad_allreduce: Eq. 5-6, A3-A5 */
+/* c_r = E4M3(fl(g_r * s_g))  (quantized once from FP32, R9)
+ * S   = sum over r = 0..N-1 of decode(c_r), binary32, rank order (exact, R12)
+ * g8  = E4M3(S): the reduced codes, on every rank (reduce-scatter + all-gather, NCCL)
+ * g_scale[t] = fl(N * s_g[t]) (Eq. 6), g_scale_inv[t] = fl(1 / g_scale[t])
+ * sat[t]     = #{i : |decode(g8[t][i])| == 448}  ("attains the maximum", R4)
+ * mu[t]     <- mu_next: halve if *skip or sat*1e5 > numel[t], else min(2, fl(mu*2^(1/1000)))
+ *              (R1-R3) — updated in place for the next step.
+ * grads as in (2).  g8: fp8lm_plan_g8_bytes bytes.  All outputs are device arrays [T]. */
+int fp8lm_grad_allreduce(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
+                         int32_t src_dtype, const float* s_g, const int32_t* skip,
+                         uint8_t* g8, float* g_scale, float* g_scale_inv, uint32_t* sat,
+                         float* mu, void* stream);
+
+/* --------------------------------- (4) fp8_adam_step: §2.2, A6 + A7 */
+/* Precision-decoupled AdamW on every tensor of the plan, JIT state scaling (R18):
+ *   g  = fl(decode(g8) * g_scale_inv[t])        (dequantize, A6)
+ *   m  = fl(decode_e4m3(m1) * m1.scale_inv[t]);  v = fl(f16(v) * v.scale_inv[t]);
+ *   w  = fl(f16(master) * master.scale_inv[t])
+ *   m' = fl(fl(b1 m) + fl(omb1 g));  v' = fl(fl(b2 v) + fl(fl(omb2 g) g))
+ *   u  = fl(m' / fl(fl(sqrt(v') * inv_bc2_sqrt) + eps));  w' = fl(fl(w decay) - fl(step_size u))
+ *   new scales from the exact amax of m', v', w' (pass 1), then encode (pass 2):
+ *   m1 <- E4M3(fl(m' * 448/A_m)),  v <- F16(fl(v' * 65504/A_v)),
+ *   master <- F16(fl(w' * 65504/A_w)),  w8 <- E4M3(fl(w' * 448/A_w))
+ *   (scale = 1 where the amax is 0); each stensor's scale/scale_inv/amax updated.
+ * If *skip != 0 nothing changes.  hp is a HOST pointer.  m1/w8 data: uint8 flat,
+ * v/master data: uint16 (FP16 bits) flat, all at the plan's offsets. */
+int fp8lm_adam_step(fp8lm_plan* plan, const uint8_t* g8, const float* g_scale_inv,
+                    const fp8lm_stensors* m1, const fp8lm_stensors* v,
+                    const fp8lm_stensors* master, const fp8lm_stensors* w8,
+                    const fp8lm_adam_hp* hp, const int32_t* skip, void* stream);
+
+/* Initial optimizer state: m1, v = zero codes with scale 1,
+ * amax 0; master / w8 JIT-encoded from the FP32 flat weights w0 (plan layout). */
+int fp8lm_state_init(fp8lm_plan* plan, const float* w0, const fp8lm_stensors* m1,
+                     const fp8lm_stensors* v, const fp8lm_stensors* master,
+                     const fp8lm_stensors* w8, void* stream);
+
+/* ------------------------------------------------------- launch tracing (auxiliary) */
+/* Host: when enabled, every kernel, memset and NCCL call the library enqueues is
+ * bracketed by CUDA events on its stream.  fp8lm_prof_enable(1) starts a new window
+ * (clears records), (0) stops recording.  fp8lm_prof_ids() = number of trace ids;
+ * fp8lm_prof_read(id, ...) synchronises the recorded events and returns the name,
+ * number of launches and summed device milliseconds of that id, and whether it is a
+ * kernel of this library (is_ours = 1) rather than a memset / NCCL collective. */
+int fp8lm_prof_enable(int on);
+int fp8lm_prof_ids(void);
+int fp8lm_prof_read(int32_t id, const char** name, int64_t* launches, double* total_ms,
+                    int32_t* is_ours);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FP8LM_H */

@@ -1,0 +1,366 @@
+"""Thin ctypes binding over libfp8lm.so (include/fp8lm.h).
+
+Argument marshalling only: PyTorch allocates device memory and supplies the stream
+(and torch.distributed bootstraps the NCCL unique id); every step of the hot path
+runs in the library's sm_100a kernels or in NCCL.  There is NO CPU fallback: if the
+shared library is missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfp8lm.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2310_18313_b200.build` "
+        "(or __graft_entry__.build()); there is no fallback path")
+
+lib = C.CDLL(LIB_PATH)
+
+# ------------------------------------------------------------------ constants (fp8lm.h)
+OK, EINVAL, ECUDA, ENCCL, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4, -5
+E4M3, E5M2, F16, BF16, F32 = 0, 1, 2, 3, 4
+MODE_LOCAL, MODE_SIMULATED, MODE_NCCL = 0, 1, 2
+ALIGN_ELEMS = 64
+MAX_SIM_RANKS = 16
+
+_p = C.c_void_p
+_i32, _i64, _u64, _f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+
+
+class AdamHP(C.Structure):
+    _fields_ = [(n, C.c_float) for n in ("beta1", "beta2", "one_minus_beta1", "one_minus_beta2",
+                                          "eps", "decay", "step_size", "inv_bc2_sqrt")]
+
+
+class STensors(C.Structure):
+    _fields_ = [("data", _p), ("scale", _p), ("scale_inv", _p), ("amax", _p)]
+
+
+def _sig(name, res, *args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_sig("fp8lm_version", C.c_int)
+_sig("fp8lm_last_error", C.c_char_p)
+_sig("fp8lm_has_nccl", C.c_int)
+_sig("fp8lm_adam_hp_make", C.c_int, _f64, _f64, _f64, _f64, _f64, _i64, C.POINTER(AdamHP))
+_sig("fp8lm_zero_plan", C.c_int, _i32, C.POINTER(_i64), _i32, C.POINTER(_i32), C.POINTER(_i64))
+_sig("fp8lm_comm_unique_id", C.c_int, C.POINTER(C.c_uint8))
+_sig("fp8lm_comm_init", C.c_int, _i32, _i32, C.POINTER(C.c_uint8), C.POINTER(_p))
+_sig("fp8lm_comm_destroy", C.c_int, _p)
+_sig("fp8lm_plan_create", C.c_int, _i32, C.POINTER(_i64), _i32, _i32, _i32, C.POINTER(_p))
+_sig("fp8lm_plan_destroy", C.c_int, _p)
+_sig("fp8lm_plan_offset", _i64, _p, _i32)
+_sig("fp8lm_plan_total", _i64, _p)
+_sig("fp8lm_plan_g8_bytes", _i64, _p)
+_sig("fp8lm_plan_shard_bytes", _i64, _p)
+_sig("fp8lm_plan_shard_begin", _i64, _p, _i32)
+_sig("fp8lm_plan_workspace_bytes", C.c_size_t, _p)
+_sig("fp8lm_plan_bind", C.c_int, _p, _p, C.c_size_t, _p)
+_sig("fp8lm_quantize", C.c_int, _p, _i32, _i64, _i32, _p, _p, _p, _p, _i32, _p, _p)
+_sig("fp8lm_dequantize", C.c_int, _p, _i32, _i64, _p, _p, _p)
+_sig("fp8lm_amax_scale_sync", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p)
+_sig("fp8lm_grad_allreduce", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p)
+_sig("fp8lm_adam_step", C.c_int, _p, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
+     C.POINTER(STensors), C.POINTER(STensors), C.POINTER(AdamHP), _p, _p)
+_sig("fp8lm_prof_enable", C.c_int, C.c_int)
+_sig("fp8lm_prof_ids", C.c_int)
+_sig("fp8lm_prof_read", C.c_int, _i32, C.POINTER(C.c_char_p), C.POINTER(_i64), C.POINTER(C.c_double),
+     C.POINTER(_i32))
+_sig("fp8lm_state_init", C.c_int, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
+     C.POINTER(STensors), C.POINTER(STensors), _p)
+
+
+class FP8LMError(RuntimeError):
+    pass
+
+
+def _check(rc: int, what: str):
+    if rc != OK:
+        msg = lib.fp8lm_last_error().decode(errors="replace")
+        raise FP8LMError(f"{what} failed ({rc}): {msg}")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.bfloat16:
+        return BF16
+    raise TypeError(f"gradients must be float32 or bfloat16, got {t.dtype}")
+
+
+# ------------------------------------------------------------------ host helpers
+def version() -> int:
+    return lib.fp8lm_version()
+
+
+def has_nccl() -> bool:
+    return bool(lib.fp8lm_has_nccl())
+
+
+def adam_hp(lr: float, step: int, beta1: float = 0.9, beta2: float = 0.95, eps: float = 1e-8,
+            weight_decay: float = 0.1) -> AdamHP:
+    """fp8lm_adam_hp_make (R24): scalars in double, rounded once to float."""
+    hp = AdamHP()
+    _check(lib.fp8lm_adam_hp_make(lr, beta1, beta2, eps, weight_decay, step, C.byref(hp)),
+           "fp8lm_adam_hp_make")
+    return hp
+
+
+def zero_plan(numels: Sequence[int], nranks: int):
+    """Alg. 1 -> (owner[T], load[nranks])."""
+    T = len(numels)
+    arr = (_i64 * max(T, 1))(*numels)
+    owner = (_i32 * max(T, 1))()
+    load = (_i64 * nranks)()
+    _check(lib.fp8lm_zero_plan(T, arr, nranks, owner, load), "fp8lm_zero_plan")
+    return list(owner)[:T], list(load)
+
+
+def prof_enable(on: bool = True):
+    """Start (True) / stop (False) the library's per-launch CUDA-event tracing."""
+    lib.fp8lm_prof_enable(1 if on else 0)
+
+
+def prof_read():
+    """-> {name: dict(launches, ms, ours)} for every id with at least one launch."""
+    out = {}
+    for i in range(lib.fp8lm_prof_ids()):
+        name, n, ms, ours = C.c_char_p(), _i64(), C.c_double(), _i32()
+        _check(lib.fp8lm_prof_read(i, C.byref(name), C.byref(n), C.byref(ms), C.byref(ours)),
+               "fp8lm_prof_read")
+        if n.value:
+            out[name.value.decode()] = dict(launches=n.value, ms=ms.value, ours=bool(ours.value))
+    return out
+
+
+# ------------------------------------------------------------------ communicator
+class Comm:
+    """An NCCL communicator owned by the library, bootstrapped over torch.distributed."""
+
+    def __init__(self, nranks: int, rank: int, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = _p()
+        _check(lib.fp8lm_comm_init(nranks, rank, buf, C.byref(h)), "fp8lm_comm_init")
+        self.handle = h
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib.fp8lm_comm_unique_id(buf), "fp8lm_comm_unique_id")
+        return bytes(buf)
+
+    @classmethod
+    def from_torch_distributed(cls, group=None) -> "Comm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj: List[Optional[bytes]] = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(world, rank, obj[0])
+
+    def close(self):
+        if self.handle:
+            lib.fp8lm_comm_destroy(self.handle)
+            self.handle = None
+
+
+# ------------------------------------------------------------------ plan
+class Plan:
+    """Flat layout of T tensors + bound device workspace (fp8lm_plan_*)."""
+
+    def __init__(self, numels: Sequence[int], mode: int = MODE_LOCAL, nranks: int = 1, rank: int = 0,
+                 device="cuda", stream=None):
+        self.numels = [int(n) for n in numels]
+        self.T = len(self.numels)
+        self.mode, self.nranks, self.rank = mode, nranks, rank
+        arr = (_i64 * max(self.T, 1))(*self.numels)
+        h = _p()
+        _check(lib.fp8lm_plan_create(self.T, arr, mode, nranks, rank, C.byref(h)), "fp8lm_plan_create")
+        self.handle = h
+        self.offsets = [lib.fp8lm_plan_offset(h, t) for t in range(self.T)]
+        self.total = lib.fp8lm_plan_total(h)
+        self.g8_bytes = lib.fp8lm_plan_g8_bytes(h)
+        self.shard_bytes = lib.fp8lm_plan_shard_bytes(h)
+        self.ws_bytes = lib.fp8lm_plan_workspace_bytes(h)
+        self.device = torch.device(device)
+        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=self.device)
+        _check(lib.fp8lm_plan_bind(h, _ptr(self.ws), self.ws.numel(), _stream(stream)), "fp8lm_plan_bind")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            lib.fp8lm_plan_destroy(h)
+            self.handle = None
+
+    def shard_begin(self, rank: int) -> int:
+        return lib.fp8lm_plan_shard_begin(self.handle, rank)
+
+    # flat buffers in plan layout
+    def flat(self, dtype, nbytes_like_g8: bool = False) -> torch.Tensor:
+        n = self.g8_bytes if nbytes_like_g8 else self.total
+        return torch.zeros(max(n, 1), dtype=dtype, device=self.device)
+
+    def views(self, flat: torch.Tensor, shapes=None) -> List[torch.Tensor]:
+        out = []
+        for t in range(self.T):
+            v = flat[self.offsets[t]: self.offsets[t] + self.numels[t]]
+            out.append(v.view(shapes[t]) if shapes is not None else v)
+        return out
+
+    def gather(self, flat: torch.Tensor, t: int) -> torch.Tensor:
+        return flat[self.offsets[t]: self.offsets[t] + self.numels[t]]
+
+
+class STensorSet:
+    """T scaling tensors packed flat: data + scale / scale_inv / amax [T]."""
+
+    def __init__(self, plan: Plan, dtype: torch.dtype):
+        self.data = plan.flat(dtype)
+        dev = plan.device
+        self.scale = torch.ones(max(plan.T, 1), dtype=torch.float32, device=dev)
+        self.scale_inv = torch.ones(max(plan.T, 1), dtype=torch.float32, device=dev)
+        self.amax = torch.zeros(max(plan.T, 1), dtype=torch.float32, device=dev)
+
+    def c(self) -> STensors:
+        return STensors(self.data.data_ptr(), self.scale.data_ptr(), self.scale_inv.data_ptr(),
+                        self.amax.data_ptr())
+
+
+class OptimizerState:
+    """6 B/param FP8 optimizer state (Eq. 8) + the E4M3 weight copy."""
+
+    def __init__(self, plan: Plan):
+        self.m1 = STensorSet(plan, torch.uint8)        # E4M3
+        self.v = STensorSet(plan, torch.float16)       # FP16 (scaled, R17)
+        self.master = STensorSet(plan, torch.float16)  # FP16 (scaled)
+        self.w8 = STensorSet(plan, torch.uint8)        # E4M3 weight copy
+
+    def tensors(self):
+        return dict(m1=self.m1, v=self.v, master=self.master, w8=self.w8)
+
+
+# ------------------------------------------------------------------ the four calls
+def fp8_quantize(src: torch.Tensor, fmt: int = E4M3, jit: bool = True, scale: torch.Tensor = None,
+                 out: torch.Tensor = None, count_sat: bool = False, stream=None):
+    """fp8lm_quantize on one tensor -> (codes, scale, scale_inv, amax, sat)."""
+    src = src.contiguous()
+    n = src.numel()
+    dev = src.device
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint8 if fmt != F16 else torch.float16, device=dev)
+    if scale is None:
+        scale = torch.ones(1, dtype=torch.float32, device=dev)
+    scale_inv = torch.ones(1, dtype=torch.float32, device=dev)
+    amax = torch.zeros(1, dtype=torch.float32, device=dev)
+    sat = torch.zeros(1, dtype=torch.int32, device=dev) if count_sat else None
+    _check(lib.fp8lm_quantize(_ptr(src), _dtype_code(src), n, fmt, _ptr(out), _ptr(scale),
+                              _ptr(scale_inv), _ptr(amax), 1 if jit else 0, _ptr(sat), _stream(stream)),
+           "fp8lm_quantize")
+    return out, scale, scale_inv, amax, sat
+
+
+def fp8_dequantize(codes: torch.Tensor, fmt: int, scale_inv: torch.Tensor, stream=None):
+    out = torch.empty(codes.numel(), dtype=torch.float32, device=codes.device)
+    _check(lib.fp8lm_dequantize(_ptr(codes), fmt, codes.numel(), _ptr(scale_inv), _ptr(out),
+                                _stream(stream)), "fp8lm_dequantize")
+    return out
+
+
+def _grads_arg(plan: Plan, grads):
+    """mode SIMULATED: a list of flat per-rank buffers -> host pointer array."""
+    if plan.mode == MODE_SIMULATED:
+        assert len(grads) == plan.nranks
+        arr = (_p * plan.nranks)(*[g.data_ptr() for g in grads])
+        return C.cast(arr, _p), _dtype_code(grads[0]), arr
+    return _ptr(grads), _dtype_code(grads), None
+
+
+def amax_scale_sync(plan: Plan, grads, mu: torch.Tensor, amax_out: torch.Tensor, s_g: torch.Tensor,
+                    skip: torch.Tensor, comm: Comm = None, stream=None):
+    g, dt, keep = _grads_arg(plan, grads)
+    _check(lib.fp8lm_amax_scale_sync(plan.handle, comm.handle if comm else None, g, dt, _ptr(mu),
+                                     _ptr(amax_out), _ptr(s_g), _ptr(skip), _stream(stream)),
+           "fp8lm_amax_scale_sync")
+    del keep
+
+
+def fp8_grad_allreduce(plan: Plan, grads, s_g: torch.Tensor, skip: torch.Tensor, g8: torch.Tensor,
+                       g_scale: torch.Tensor, g_scale_inv: torch.Tensor, sat: torch.Tensor,
+                       mu: torch.Tensor, comm: Comm = None, stream=None):
+    g, dt, keep = _grads_arg(plan, grads)
+    _check(lib.fp8lm_grad_allreduce(plan.handle, comm.handle if comm else None, g, dt, _ptr(s_g),
+                                    _ptr(skip), _ptr(g8), _ptr(g_scale), _ptr(g_scale_inv),
+                                    _ptr(sat), _ptr(mu), _stream(stream)),
+           "fp8lm_grad_allreduce")
+    del keep
+
+
+def fp8_adam_step(plan: Plan, g8: torch.Tensor, g_scale_inv: torch.Tensor, st: OptimizerState,
+                  hp: AdamHP, skip: torch.Tensor, stream=None):
+    m1, v, w, w8 = st.m1.c(), st.v.c(), st.master.c(), st.w8.c()
+    _check(lib.fp8lm_adam_step(plan.handle, _ptr(g8), _ptr(g_scale_inv), C.byref(m1), C.byref(v),
+                               C.byref(w), C.byref(w8), C.byref(hp), _ptr(skip), _stream(stream)),
+           "fp8lm_adam_step")
+
+
+def state_init(plan: Plan, w0_flat: torch.Tensor, st: OptimizerState, stream=None):
+    m1, v, w, w8 = st.m1.c(), st.v.c(), st.master.c(), st.w8.c()
+    _check(lib.fp8lm_state_init(plan.handle, _ptr(w0_flat), C.byref(m1), C.byref(v), C.byref(w),
+                                C.byref(w8), _stream(stream)), "fp8lm_state_init")
+
+
+# ------------------------------------------------------------------ the whole DP step
+class FP8DataParallel:
+    """The full hot path (§8a rows A1-A7) for one rank: owns the per-step device scalars.
+
+    step(grads, lr): amax_scale_sync -> fp8_grad_allreduce -> fp8_adam_step, all on the
+    current stream, no host synchronisation.  After it, .w8 (E4M3 weight copy) and its
+    scale feed the next forward pass; .mu is already updated for the next step."""
+
+    def __init__(self, plan: Plan, w0_flat: torch.Tensor, comm: Comm = None, lr: float = 3e-4,
+                 betas=(0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.1):
+        self.plan, self.comm = plan, comm
+        dev = plan.device
+        T = max(plan.T, 1)
+        nsim = plan.nranks if plan.mode == MODE_SIMULATED else 1
+        self.mu = torch.ones(T, dtype=torch.float32, device=dev)
+        self.amax = torch.zeros(nsim * T, dtype=torch.float32, device=dev)
+        self.s_g = torch.zeros(T, dtype=torch.float32, device=dev)
+        self.skip = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.g8 = plan.flat(torch.uint8, nbytes_like_g8=True)
+        self.g_scale = torch.zeros(T, dtype=torch.float32, device=dev)
+        self.g_scale_inv = torch.zeros(T, dtype=torch.float32, device=dev)
+        self.sat = torch.zeros(T, dtype=torch.int32, device=dev)
+        self.state = OptimizerState(plan)
+        state_init(plan, w0_flat, self.state)
+        self.lr, self.betas, self.eps, self.wd = lr, betas, eps, weight_decay
+        self.t = 0
+
+    def step(self, grads, lr: float = None, stream=None):
+        self.t += 1
+        hp = adam_hp(self.lr if lr is None else lr, self.t, self.betas[0], self.betas[1], self.eps, self.wd)
+        amax_scale_sync(self.plan, grads, self.mu, self.amax, self.s_g, self.skip, self.comm, stream)
+        fp8_grad_allreduce(self.plan, grads, self.s_g, self.skip, self.g8, self.g_scale,
+                           self.g_scale_inv, self.sat, self.mu, self.comm, stream)
+        fp8_adam_step(self.plan, self.g8, self.g_scale_inv, self.state, hp, self.skip, stream)

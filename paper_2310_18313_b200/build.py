@@ -1,0 +1,82 @@
+"""Build libfp8lm.so in-tree with nvcc for sm_100a (no JIT, no torch extension cache).
+
+    python -m paper_2310_18313_b200.build          # or __graft_entry__.build()
+
+Flags: -gencode arch=compute_100a,code=sm_100a (arch-specific: the packed FP8 cvt and
+256-bit ld/st are sm_100a instructions); -fmad=false + IEEE div/sqrt so that every
+binary32 rounding matches the oracle's (R16); -lineinfo for ncu source
+correlation.  NCCL: the torch-bundled libnccl.so.2 (the same library torch loads).
+"""
+from __future__ import annotations
+
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libfp8lm.so")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dirs():
+    try:
+        import nvidia.nccl as nn
+        base = list(nn.__path__)[0]
+    except Exception:
+        return None, None
+    inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+    if os.path.exists(os.path.join(inc, "nccl.h")) and glob.glob(os.path.join(lib, "libnccl.so*")):
+        return inc, lib
+    return None, None
+
+
+def nvcc():
+    for c in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+
+
+def needs_rebuild() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+    deps.append(os.path.join(ROOT, "include", "fp8lm.h"))
+    deps.append(os.path.abspath(__file__))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_rebuild():
+        return LIB
+    inc, lib = nccl_dirs()
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
+           "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
+           "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared",
+           "-I", os.path.join(ROOT, "include")]
+    if inc:
+        cmd += ["-DFP8LM_WITH_NCCL", "-I", inc]
+    cmd += sources()
+    if lib:
+        cmd += ["-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
+    cmd += ["-o", LIB + ".tmp"]
+    if verbose:
+        print(" ".join(cmd))
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

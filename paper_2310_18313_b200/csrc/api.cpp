@@ -1,0 +1,495 @@
+// api.cpp — the C ABI declared in include/fp8lm.h: argument checking, the flat-layout
+// plan, the NCCL communicator, and the sequencing of kernels + collectives for the
+// four hot-path calls.  Every step of the hot path runs in kernels.cu or in NCCL; this
+// file only validates arguments and enqueues work on the caller's stream.
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#ifdef FP8LM_WITH_NCCL
+#include <nccl.h>
+#endif
+
+#include "config.h"
+#include "internal.h"
+
+using namespace fp8lm;
+
+// ---------------------------------------------------------------- error plumbing
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(FP8LM_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_));            \
+  } while (0)
+
+#ifdef FP8LM_WITH_NCCL
+#define NCCL_TRY(expr)                                                              \
+  do {                                                                              \
+    ncclResult_t r_ = (expr);                                                       \
+    if (r_ != ncclSuccess)                                                          \
+      return fail(FP8LM_ENCCL, "%s: %s", #expr, ncclGetErrorString(r_));            \
+  } while (0)
+#endif
+
+struct fp8lm_comm {
+#ifdef FP8LM_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  int32_t nranks = 0;
+  int32_t rank = 0;
+};
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+static inline bool aligned(const void* p, size_t a) {
+  return (reinterpret_cast<uintptr_t>(p) % a) == 0;
+}
+
+extern "C" {
+
+int fp8lm_version(void) { return FP8LM_ABI_VERSION; }
+const char* fp8lm_last_error(void) { return g_err.c_str(); }
+int fp8lm_has_nccl(void) {
+#ifdef FP8LM_WITH_NCCL
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+// ---------------------------------------------------------------- host scalars (R24)
+int fp8lm_adam_hp_make(double lr, double beta1, double beta2, double eps, double weight_decay,
+                       int64_t step, fp8lm_adam_hp* out) {
+  if (!out) return fail(FP8LM_EINVAL, "adam_hp_make: out is NULL");
+  if (step < 1) return fail(FP8LM_EINVAL, "adam_hp_make: step must be >= 1 (got %lld)", (long long)step);
+  if (!std::isfinite(lr) || !std::isfinite(beta1) || !std::isfinite(beta2) || !std::isfinite(eps) ||
+      !std::isfinite(weight_decay) || beta1 < 0 || beta1 >= 1 || beta2 < 0 || beta2 >= 1)
+    return fail(FP8LM_EINVAL, "adam_hp_make: invalid hyper-parameters");
+  out->beta1 = (float)beta1;
+  out->beta2 = (float)beta2;
+  out->one_minus_beta1 = (float)(1.0 - beta1);
+  out->one_minus_beta2 = (float)(1.0 - beta2);
+  out->eps = (float)eps;
+  out->decay = (float)(1.0 - lr * weight_decay);
+  out->step_size = (float)(lr / (1.0 - std::pow(beta1, (double)step)));
+  out->inv_bc2_sqrt = (float)(1.0 / std::sqrt(1.0 - std::pow(beta2, (double)step)));
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- Alg. 1
+int fp8lm_zero_plan(int32_t T, const int64_t* numels, int32_t nranks, int32_t* owner_out,
+                    int64_t* load_out) {
+  if (T < 0 || nranks < 1) return fail(FP8LM_EINVAL, "zero_plan: T=%d nranks=%d", T, nranks);
+  if (T > 0 && (!numels || !owner_out)) return fail(FP8LM_EINVAL, "zero_plan: NULL array");
+  if (!load_out) return fail(FP8LM_EINVAL, "zero_plan: load_out is NULL");
+  // line 1: sort by size, descending; equal sizes keep ascending original index (R21)
+  std::vector<int32_t> order(T);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return numels[a] > numels[b]; });
+  // line 2: u_j = 0
+  for (int j = 0; j < nranks; ++j) load_out[j] = 0;
+  for (int32_t i : order) {                       // line 3
+    int j = 0;                                    // line 4: argmin u_j, lowest index on ties
+    for (int k = 1; k < nranks; ++k)
+      if (load_out[k] < load_out[j]) j = k;
+    owner_out[i] = j;                             // line 5
+    load_out[j] += numels[i];                     // line 6
+  }
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- communicator
+int fp8lm_comm_unique_id(uint8_t* id_out) {
+#ifdef FP8LM_WITH_NCCL
+  if (!id_out) return fail(FP8LM_EINVAL, "comm_unique_id: NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof id);
+  return FP8LM_OK;
+#else
+  (void)id_out;
+  return fail(FP8LM_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+int fp8lm_comm_init(int32_t nranks, int32_t rank, const uint8_t* id, fp8lm_comm** out) {
+#ifdef FP8LM_WITH_NCCL
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(FP8LM_EINVAL, "comm_init: bad arguments (nranks=%d rank=%d)", nranks, rank);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  auto* c = new fp8lm_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(FP8LM_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return FP8LM_OK;
+#else
+  (void)nranks; (void)rank; (void)id; (void)out;
+  return fail(FP8LM_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+int fp8lm_comm_destroy(fp8lm_comm* comm) {
+  if (!comm) return FP8LM_OK;
+#ifdef FP8LM_WITH_NCCL
+  if (comm->comm) {
+    ncclCommFinalize(comm->comm);
+    ncclCommDestroy(comm->comm);
+  }
+#endif
+  delete comm;
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- plan
+int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nranks,
+                      int32_t rank, fp8lm_plan** out) {
+  if (!out) return fail(FP8LM_EINVAL, "plan_create: out is NULL");
+  if (T < 0 || (T > 0 && !numels)) return fail(FP8LM_EINVAL, "plan_create: bad T / numels");
+  if (mode < FP8LM_MODE_LOCAL || mode > FP8LM_MODE_NCCL)
+    return fail(FP8LM_EINVAL, "plan_create: bad mode %d", mode);
+  if (nranks < 1) return fail(FP8LM_EINVAL, "plan_create: nranks must be >= 1");
+  if (mode == FP8LM_MODE_LOCAL && nranks != 1)
+    return fail(FP8LM_EINVAL, "plan_create: mode LOCAL needs nranks == 1");
+  if (mode == FP8LM_MODE_SIMULATED && nranks > FP8LM_MAX_SIM_RANKS)
+    return fail(FP8LM_EINVAL, "plan_create: at most %d simulated ranks", FP8LM_MAX_SIM_RANKS);
+  if (mode == FP8LM_MODE_NCCL && (rank < 0 || rank >= nranks))
+    return fail(FP8LM_EINVAL, "plan_create: rank %d out of range", rank);
+  for (int t = 0; t < T; ++t)
+    if (numels[t] < 0) return fail(FP8LM_EINVAL, "plan_create: numel[%d] < 0", t);
+
+  auto* p = new fp8lm_plan();
+  p->T = T;
+  p->mode = mode;
+  p->nranks = nranks;
+  p->rank = mode == FP8LM_MODE_NCCL ? rank : 0;
+  p->numel.assign(numels, numels + T);
+  p->offset.resize(T);
+  p->item_start.resize(T + 1);
+  int64_t run = 0, items = 0;
+  for (int t = 0; t < T; ++t) {
+    p->offset[t] = run;
+    run += round_up(p->numel[t], FP8LM_ALIGN_ELEMS);
+    p->item_start[t] = items;
+    items += (p->numel[t] + kChunk - 1) / kChunk;
+  }
+  p->item_start[T] = items;
+  p->total = run;
+  p->g8_bytes = run;
+  if (mode == FP8LM_MODE_NCCL) {
+    // reduce-scatter shards: N contiguous byte ranges of the flat code buffer, each a
+    // multiple of 64 bytes so that every shard item starts 16-byte aligned
+    const int64_t N = nranks;
+    p->shard = std::max<int64_t>(round_up((run + N - 1) / N, FP8LM_ALIGN_ELEMS), FP8LM_ALIGN_ELEMS);
+    p->g8_bytes = p->shard * N;
+    const int64_t lo = p->shard * p->rank, hi = lo + p->shard;
+    for (int t = 0; t < T; ++t) {
+      const int64_t a = std::max(lo, p->offset[t]);
+      const int64_t b = std::min(hi, p->offset[t] + p->numel[t]);
+      for (int64_t x = a; x < b; x += kChunk)
+        p->shard_items.push_back(ShardItem{x, t, (int32_t)std::min<int64_t>(kChunk, b - x)});
+    }
+  }
+  // workspace layout
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (size_t)round_up((int64_t)bytes, 256); return o; };
+  const int nsim = mode == FP8LM_MODE_SIMULATED ? nranks : 1;
+  p->off_numel = take(sizeof(int64_t) * std::max(T, 1));
+  p->off_offset = take(sizeof(int64_t) * std::max(T, 1));
+  p->off_item_start = take(sizeof(int64_t) * (T + 1));
+  p->off_shard_items = take(sizeof(ShardItem) * std::max<size_t>(p->shard_items.size(), 1));
+  p->off_acc_amax = take(sizeof(uint32_t) * std::max(nsim * T, 1));
+  p->off_acc_state = take(sizeof(uint32_t) * std::max(3 * T, 1));
+  p->off_sat_part = take(sizeof(uint32_t) * std::max(T, 1));
+  p->off_acc_end = off;
+  if (mode == FP8LM_MODE_NCCL) {
+    p->off_send = take((size_t)(p->shard * nranks));
+    p->off_recv = take((size_t)(p->shard * nranks));
+  }
+  if (mode == FP8LM_MODE_SIMULATED) p->off_sim = take((size_t)(p->total * nranks));
+  p->ws_bytes = off;
+  *out = p;
+  return FP8LM_OK;
+}
+
+int fp8lm_plan_destroy(fp8lm_plan* plan) {
+  delete plan;
+  return FP8LM_OK;
+}
+
+int64_t fp8lm_plan_offset(const fp8lm_plan* p, int32_t t) {
+  if (!p || t < 0 || t >= p->T) return -1;
+  return p->offset[t];
+}
+int64_t fp8lm_plan_total(const fp8lm_plan* p) { return p ? p->total : -1; }
+int64_t fp8lm_plan_g8_bytes(const fp8lm_plan* p) { return p ? p->g8_bytes : -1; }
+int64_t fp8lm_plan_shard_bytes(const fp8lm_plan* p) { return p ? p->shard : -1; }
+int64_t fp8lm_plan_shard_begin(const fp8lm_plan* p, int32_t rank) {
+  if (!p || rank < 0 || rank >= p->nranks) return -1;
+  return p->shard * rank;
+}
+size_t fp8lm_plan_workspace_bytes(const fp8lm_plan* p) { return p ? p->ws_bytes : 0; }
+
+int fp8lm_plan_bind(fp8lm_plan* p, void* ws, size_t ws_bytes, void* stream) {
+  if (!p) return fail(FP8LM_EINVAL, "plan_bind: plan is NULL");
+  if (!ws || ws_bytes < p->ws_bytes || !aligned(ws, 256))
+    return fail(FP8LM_EWORKSPACE, "plan_bind: need %zu bytes, 256-aligned (got %zu at %p)",
+                p->ws_bytes, ws_bytes, ws);
+  uint8_t* b = static_cast<uint8_t*>(ws);
+  cudaStream_t s = S(stream);
+  if (p->T > 0) {
+    CUDA_TRY(cudaMemcpyAsync(b + p->off_numel, p->numel.data(), sizeof(int64_t) * p->T, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(b + p->off_offset, p->offset.data(), sizeof(int64_t) * p->T, cudaMemcpyHostToDevice, s));
+  }
+  CUDA_TRY(cudaMemcpyAsync(b + p->off_item_start, p->item_start.data(), sizeof(int64_t) * (p->T + 1), cudaMemcpyHostToDevice, s));
+  if (!p->shard_items.empty())
+    CUDA_TRY(cudaMemcpyAsync(b + p->off_shard_items, p->shard_items.data(), sizeof(ShardItem) * p->shard_items.size(), cudaMemcpyHostToDevice, s));
+  // accumulators (acc_amax, acc_state, sat_part: consecutive regions) must be zero at rest
+  CUDA_TRY(cudaMemsetAsync(b + p->off_acc_amax, 0, p->off_acc_end - p->off_acc_amax, s));
+  CUDA_TRY(cudaStreamSynchronize(s));   // host tables are pageable: finish before returning
+  DevPlan& d = p->dev;
+  d.T = p->T;
+  d.nranks = p->nranks;
+  d.total = p->total;
+  d.n_items = p->item_start[p->T];
+  d.numel = reinterpret_cast<const int64_t*>(b + p->off_numel);
+  d.offset = reinterpret_cast<const int64_t*>(b + p->off_offset);
+  d.item_start = reinterpret_cast<const int64_t*>(b + p->off_item_start);
+  d.shard_items = reinterpret_cast<const ShardItem*>(b + p->off_shard_items);
+  d.n_shard_items = (int64_t)p->shard_items.size();
+  d.acc_amax = reinterpret_cast<uint32_t*>(b + p->off_acc_amax);
+  d.acc_state = reinterpret_cast<uint32_t*>(b + p->off_acc_state);
+  d.sat_part = reinterpret_cast<uint32_t*>(b + p->off_sat_part);
+  d.send = p->mode == FP8LM_MODE_NCCL ? b + p->off_send : nullptr;
+  d.recv = p->mode == FP8LM_MODE_NCCL ? b + p->off_recv : nullptr;
+  d.sim_codes = p->mode == FP8LM_MODE_SIMULATED ? b + p->off_sim : nullptr;
+  p->ws = ws;
+  p->bound = true;
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- shared checks
+static int check_plan(const fp8lm_plan* p, const fp8lm_comm* comm, const char* who) {
+  if (!p) return fail(FP8LM_EINVAL, "%s: plan is NULL", who);
+  if (!p->bound) return fail(FP8LM_EWORKSPACE, "%s: plan not bound to a workspace", who);
+  if (p->mode == FP8LM_MODE_NCCL) {
+    if (!comm) return fail(FP8LM_EINVAL, "%s: mode NCCL needs a communicator", who);
+    if (comm->nranks != p->nranks || comm->rank != p->rank)
+      return fail(FP8LM_EINVAL, "%s: communicator (%d/%d) does not match plan (%d/%d)", who,
+                  comm->rank, comm->nranks, p->rank, p->nranks);
+  } else if (comm) {
+    return fail(FP8LM_EINVAL, "%s: communicator given but plan mode is not NCCL", who);
+  }
+  return FP8LM_OK;
+}
+
+// resolve the gradient source(s): SIMULATED -> host array of nranks device pointers
+static int grad_sources(const fp8lm_plan* p, const void* grads, int32_t dtype,
+                        const void** srcs, int* nsrc, const char* who) {
+  if (dtype != FP8LM_F32 && dtype != FP8LM_BF16)
+    return fail(FP8LM_EUNSUPPORTED, "%s: gradients must be F32 or BF16", who);
+  if (!grads) return fail(FP8LM_EINVAL, "%s: grads is NULL", who);
+  if (p->mode == FP8LM_MODE_SIMULATED) {
+    const void* const* arr = static_cast<const void* const*>(grads);
+    *nsrc = p->nranks;
+    for (int r = 0; r < p->nranks; ++r) srcs[r] = arr[r];
+  } else {
+    *nsrc = 1;
+    srcs[0] = grads;
+  }
+  for (int r = 0; r < *nsrc; ++r)
+    if (!srcs[r] || !aligned(srcs[r], 256))
+      return fail(FP8LM_EINVAL, "%s: gradient buffer %d is NULL or not 256-byte aligned", who, r);
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- (1) fp8_quantize
+int fp8lm_quantize(const void* src, int32_t src_dtype, int64_t n, int32_t fmt, void* dst,
+                   float* scale, float* scale_inv, float* amax, int32_t jit, uint32_t* sat_count,
+                   void* stream) {
+  if (n < 0) return fail(FP8LM_EINVAL, "quantize: n < 0");
+  if (src_dtype != FP8LM_F32 && src_dtype != FP8LM_BF16)
+    return fail(FP8LM_EUNSUPPORTED, "quantize: src dtype must be F32 or BF16");
+  if (fmt != FP8LM_E4M3 && fmt != FP8LM_E5M2 && fmt != FP8LM_F16)
+    return fail(FP8LM_EINVAL, "quantize: fmt must be E4M3, E5M2 or F16");
+  if (n > 0 && (!src || !dst)) return fail(FP8LM_EINVAL, "quantize: NULL src/dst");
+  if (!scale || (jit && (!scale_inv || !amax)))
+    return fail(FP8LM_EINVAL, "quantize: NULL scale pointers");
+  CUDA_TRY(launch_q_single(src, src_dtype, n, fmt, dst, scale, scale_inv, amax, jit, sat_count, S(stream)));
+  return FP8LM_OK;
+}
+
+int fp8lm_dequantize(const void* codes, int32_t fmt, int64_t n, const float* scale_inv,
+                     float* dst, void* stream) {
+  if (n < 0) return fail(FP8LM_EINVAL, "dequantize: n < 0");
+  if (fmt != FP8LM_E4M3 && fmt != FP8LM_E5M2 && fmt != FP8LM_F16)
+    return fail(FP8LM_EINVAL, "dequantize: fmt must be E4M3, E5M2 or F16");
+  if (n > 0 && (!codes || !dst || !scale_inv)) return fail(FP8LM_EINVAL, "dequantize: NULL pointer");
+  CUDA_TRY(launch_dq_single(codes, fmt, n, scale_inv, dst, S(stream)));
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- (2) amax_scale_sync
+int fp8lm_amax_scale_sync(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
+                          const float* mu, float* amax_out, float* s_g, int32_t* skip,
+                          void* stream) {
+  int rc = check_plan(p, comm, "amax_scale_sync");
+  if (rc) return rc;
+  const void* srcs[FP8LM_MAX_SIM_RANKS];
+  int nsrc = 0;
+  if (p->T > 0 && (rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "amax_scale_sync"))) return rc;
+  if (!mu || !amax_out || !s_g || !skip) return fail(FP8LM_EINVAL, "amax_scale_sync: NULL output");
+  cudaStream_t s = S(stream);
+  {
+    ProfScope ps_(P_MEMSET, s);
+    CUDA_TRY(cudaMemsetAsync(skip, 0, sizeof(int32_t), s));
+  }
+  if (p->T == 0) return FP8LM_OK;
+  CUDA_TRY(launch_amax(p->dev, srcs, nsrc, src_dtype, s));
+  const bool nccl = p->mode == FP8LM_MODE_NCCL;
+  CUDA_TRY(launch_scale(p->dev, nsrc, mu, amax_out, s_g, skip, !nccl, s));
+  if (nccl) {
+#ifdef FP8LM_WITH_NCCL
+    // Eq. 4: s'_g = min(s'_1, ..., s'_N) — T floats over NVLink
+    {
+      ProfScope ps_(P_NCCL_MIN, s);
+      NCCL_TRY(ncclAllReduce(s_g, s_g, (size_t)p->T, ncclFloat32, ncclMin, comm->comm, s));
+    }
+    CUDA_TRY(launch_scale_fix(p->dev, s_g, skip, s));
+#else
+    return fail(FP8LM_EUNSUPPORTED, "built without NCCL");
+#endif
+  }
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- (3) fp8_grad_allreduce
+int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
+                         const float* s_g, const int32_t* skip, uint8_t* g8, float* g_scale,
+                         float* g_scale_inv, uint32_t* sat, float* mu, void* stream) {
+  int rc = check_plan(p, comm, "grad_allreduce");
+  if (rc) return rc;
+  const void* srcs[FP8LM_MAX_SIM_RANKS];
+  int nsrc = 0;
+  if (p->T > 0 && (rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "grad_allreduce"))) return rc;
+  if (!s_g || !skip || !g_scale || !g_scale_inv || !sat || !mu)
+    return fail(FP8LM_EINVAL, "grad_allreduce: NULL scalar array");
+  if (p->T > 0 && (!g8 || !aligned(g8, 256)))
+    return fail(FP8LM_EINVAL, "grad_allreduce: g8 NULL or not 256-byte aligned");
+  cudaStream_t s = S(stream);
+  if (p->T == 0) return FP8LM_OK;
+  {
+    ProfScope ps_(P_MEMSET, s);
+    CUDA_TRY(cudaMemsetAsync(sat, 0, sizeof(uint32_t) * p->T, s));
+  }
+  const DevPlan& d = p->dev;
+  if (p->mode == FP8LM_MODE_LOCAL) {
+    // N = 1: the reduce-scatter / all-gather are the identity (A4, A5); count here
+    uint8_t* dst[1] = {g8};
+    CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, sat, s));
+  } else if (p->mode == FP8LM_MODE_SIMULATED) {
+    uint8_t* dst[FP8LM_MAX_SIM_RANKS];
+    for (int r = 0; r < nsrc; ++r) dst[r] = d.sim_codes + (int64_t)r * p->total;
+    CUDA_TRY(launch_quantize(d, srcs, dst, nsrc, src_dtype, s_g, nullptr, s));
+    CUDA_TRY(launch_reduce(d, d.sim_codes, p->total, nsrc, 0, false, g8, sat, s));
+  } else {
+#ifdef FP8LM_WITH_NCCL
+    const int64_t S_ = p->shard;
+    uint8_t* dst[1] = {d.send};
+    CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, nullptr, s));
+    // reduce-scatter transport: chunk j of the flat code buffer goes to rank j
+    {
+      ProfScope ps_(P_NCCL_A2A, s);
+      NCCL_TRY(ncclAlltoAll(d.send, d.recv, (size_t)S_, ncclUint8, comm->comm, s));
+    }
+    {
+      ProfScope ps_(P_MEMSET, s);
+      CUDA_TRY(cudaMemsetAsync(d.sat_part, 0, sizeof(uint32_t) * p->T, s));
+    }
+    CUDA_TRY(launch_reduce(d, d.recv, S_, p->nranks, S_ * p->rank, true, g8, d.sat_part, s));
+    // all-gather of the reduced shards (in place) + global saturation counts
+    {
+      ProfScope ps_(P_NCCL_AG_SUM, s);
+      NCCL_TRY(ncclGroupStart());
+      NCCL_TRY(ncclAllGather(g8 + S_ * p->rank, g8, (size_t)S_, ncclUint8, comm->comm, s));
+      NCCL_TRY(ncclAllReduce(d.sat_part, sat, (size_t)p->T, ncclUint32, ncclSum, comm->comm, s));
+      NCCL_TRY(ncclGroupEnd());
+    }
+#else
+    return fail(FP8LM_EUNSUPPORTED, "built without NCCL");
+#endif
+  }
+  CUDA_TRY(launch_allreduce_finalize(d, p->nranks, s_g, skip, sat, g_scale, g_scale_inv, mu, s));
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- (4) fp8_adam_step
+static int check_stensors(const fp8lm_plan* p, const fp8lm_stensors* x, const char* name,
+                          const char* who) {
+  if (!x) return fail(FP8LM_EINVAL, "%s: %s is NULL", who, name);
+  if (!x->scale || !x->scale_inv || !x->amax)
+    return fail(FP8LM_EINVAL, "%s: %s scalar arrays must be non-NULL", who, name);
+  if (p->T > 0 && (!x->data || !aligned(x->data, 256)))
+    return fail(FP8LM_EINVAL, "%s: %s.data NULL or not 256-byte aligned", who, name);
+  return FP8LM_OK;
+}
+
+int fp8lm_adam_step(fp8lm_plan* p, const uint8_t* g8, const float* g_scale_inv,
+                    const fp8lm_stensors* m1, const fp8lm_stensors* v,
+                    const fp8lm_stensors* master, const fp8lm_stensors* w8,
+                    const fp8lm_adam_hp* hp, const int32_t* skip, void* stream) {
+  if (!p) return fail(FP8LM_EINVAL, "adam_step: plan is NULL");
+  if (!p->bound) return fail(FP8LM_EWORKSPACE, "adam_step: plan not bound");
+  int rc;
+  if ((rc = check_stensors(p, m1, "m1", "adam_step")) || (rc = check_stensors(p, v, "v", "adam_step")) ||
+      (rc = check_stensors(p, master, "master", "adam_step")) || (rc = check_stensors(p, w8, "w8", "adam_step")))
+    return rc;
+  if (!hp || !skip || !g_scale_inv) return fail(FP8LM_EINVAL, "adam_step: NULL hp / skip / g_scale_inv");
+  if (p->T > 0 && (!g8 || !aligned(g8, 256))) return fail(FP8LM_EINVAL, "adam_step: g8 NULL or misaligned");
+  CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream)));
+  return FP8LM_OK;
+}
+
+int fp8lm_state_init(fp8lm_plan* p, const float* w0, const fp8lm_stensors* m1,
+                     const fp8lm_stensors* v, const fp8lm_stensors* master,
+                     const fp8lm_stensors* w8, void* stream) {
+  if (!p) return fail(FP8LM_EINVAL, "state_init: plan is NULL");
+  if (!p->bound) return fail(FP8LM_EWORKSPACE, "state_init: plan not bound");
+  int rc;
+  if ((rc = check_stensors(p, m1, "m1", "state_init")) || (rc = check_stensors(p, v, "v", "state_init")) ||
+      (rc = check_stensors(p, master, "master", "state_init")) || (rc = check_stensors(p, w8, "w8", "state_init")))
+    return rc;
+  if (p->T > 0 && (!w0 || !aligned(w0, 256))) return fail(FP8LM_EINVAL, "state_init: w0 NULL or misaligned");
+  CUDA_TRY(launch_state_init(p->dev, w0, *m1, *v, *master, *w8, S(stream)));
+  return FP8LM_OK;
+}
+
+}  // extern "C"

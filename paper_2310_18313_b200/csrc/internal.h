@@ -1,0 +1,110 @@
+// internal.h — host-side structures shared by the C-ABI layer (api.cpp) and the
+// kernel launchers (kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/fp8lm.h"
+
+namespace fp8lm {
+
+// one reduce-scatter work item: bytes [pos, pos+len) of tensor t (global flat coords)
+struct ShardItem {
+  int64_t pos;
+  int32_t t;
+  int32_t len;
+};
+
+// device views of the plan tables inside the caller's workspace
+struct DevPlan {
+  int32_t T;
+  int32_t nranks;
+  int64_t total;            // elements of each flat buffer
+  int64_t n_items;          // full-tensor work items
+  const int64_t* numel;     // [T]
+  const int64_t* offset;    // [T]
+  const int64_t* item_start;// [T+1]
+  const ShardItem* shard_items;
+  int64_t n_shard_items;
+  uint32_t* acc_amax;       // [nsim*T]  float bits, atomicMax accumulators (zero at rest)
+  uint32_t* acc_state;      // [3*T]     amax of m', v', w' (zero at rest)
+  uint32_t* sat_part;       // [T]       per-shard saturation counts (NCCL)
+  uint8_t* send;            // [N*S]     NCCL send buffer (quantized codes, flat)
+  uint8_t* recv;            // [N*S]     NCCL all-to-all receive buffer
+  uint8_t* sim_codes;       // [nsim*total] simulated ranks' quantized codes
+};
+
+}  // namespace fp8lm
+
+struct fp8lm_plan {
+  int32_t T = 0;
+  int32_t mode = 0;
+  int32_t nranks = 1;
+  int32_t rank = 0;
+  std::vector<int64_t> numel, offset, item_start;
+  std::vector<fp8lm::ShardItem> shard_items;
+  int64_t total = 0;        // elements per flat buffer
+  int64_t shard = 0;        // S bytes (NCCL)
+  int64_t g8_bytes = 0;
+  // workspace layout (byte offsets)
+  size_t off_numel = 0, off_offset = 0, off_item_start = 0, off_shard_items = 0;
+  size_t off_acc_amax = 0, off_acc_state = 0, off_sat_part = 0, off_acc_end = 0;
+  size_t off_send = 0, off_recv = 0, off_sim = 0, ws_bytes = 0;
+  void* ws = nullptr;
+  fp8lm::DevPlan dev{};
+  bool bound = false;
+};
+
+namespace fp8lm {
+// ------------------------------------------------------------------ launch tracing
+// When enabled (fp8lm_prof_enable), every kernel / collective the library enqueues is
+// bracketed by two CUDA events on its own stream; fp8lm_prof_read aggregates the
+// durations per name.  Used by bench.py for the per-kernel roofline and launch count.
+enum ProfId : int {
+  P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
+  P_ADAM_FINALIZE, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
+  P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_COUNT
+};
+bool prof_on();
+struct ProfScope {
+  int id;
+  cudaStream_t s;
+  void* a = nullptr;
+  ProfScope(int id_, cudaStream_t s_);
+  ~ProfScope();
+};
+
+// kernel launchers (kernels.cu); return cudaError_t of the launch
+cudaError_t launch_amax(const DevPlan& p, const void* const* srcs, int nsrc, int src_dtype,
+                        cudaStream_t s);
+cudaError_t launch_scale(const DevPlan& p, int nsrc, const float* mu, float* amax_out,
+                         float* s_out, int32_t* skip, bool finalize, cudaStream_t s);
+cudaError_t launch_scale_fix(const DevPlan& p, float* s_g, int32_t* skip, cudaStream_t s);
+cudaError_t launch_quantize(const DevPlan& p, const void* const* srcs, uint8_t* const* dsts,
+                            int nsrc, int src_dtype, const float* s_g, uint32_t* sat,
+                            cudaStream_t s);
+cudaError_t launch_reduce(const DevPlan& p, const uint8_t* base, int64_t stride, int nsrc,
+                          int64_t shift, bool shard_items, uint8_t* dst, uint32_t* sat,
+                          cudaStream_t s);
+cudaError_t launch_allreduce_finalize(const DevPlan& p, int nranks, const float* s_g,
+                                      const int32_t* skip, const uint32_t* sat, float* g_scale,
+                                      float* g_scale_inv, float* mu, cudaStream_t s);
+cudaError_t launch_adam(const DevPlan& p, const uint8_t* g8, const float* g_sinv,
+                        const fp8lm_stensors& m1, const fp8lm_stensors& v,
+                        const fp8lm_stensors& w, const fp8lm_stensors& w8,
+                        const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s);
+cudaError_t launch_state_init(const DevPlan& p, const float* w0, const fp8lm_stensors& m1,
+                              const fp8lm_stensors& v, const fp8lm_stensors& w,
+                              const fp8lm_stensors& w8, cudaStream_t s);
+// single-tensor codec (fp8lm_quantize / fp8lm_dequantize)
+cudaError_t launch_q_single(const void* src, int src_dtype, int64_t n, int fmt, void* dst,
+                            float* scale, float* scale_inv, float* amax, int jit,
+                            uint32_t* sat, cudaStream_t s);
+cudaError_t launch_dq_single(const void* codes, int fmt, int64_t n, const float* scale_inv,
+                             float* dst, cudaStream_t s);
+int num_sms();
+}  // namespace fp8lm

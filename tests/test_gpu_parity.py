@@ -1,0 +1,207 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element,
+on the same seeded inputs.  Bar (BASELINE.json north_star): FP8 codes, FP16 state bits,
+scales, amax, mu, sat bit-exact; the pinned binary32 sequence (R16) makes that
+achievable, so the tolerances of the north star are not used as a licence.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.conftest import gpu_available
+from tests import _gpu_ref as R
+from tests.test_oracle_codec import _probe_inputs
+
+from oracle import adam as OA
+from oracle import pipeline as OP
+from oracle import step as OS
+from oracle.codec import E4M3, E5M2, FP16, decode, encode
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+F32 = np.float32
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def B():
+    import paper_2310_18313_b200 as b
+    return b
+
+
+# ----------------------------------------------------------------- codec (App. A)
+@pytest.mark.parametrize("fmt", ["e4m3", "e5m2", "f16"])
+def test_codec_unit_scale_vs_oracle(B, fmt):
+    """Device encode of 1M random + every (exponent x top-5-mantissa x low-bit pattern)
+    binary32 input, unit scale, vs the oracle: bit-exact (NaN: class only)."""
+    fcode = {"e4m3": B.E4M3, "e5m2": B.E5M2, "f16": B.F16}[fmt]
+    ofmt = {"e4m3": E4M3, "e5m2": E5M2, "f16": FP16}[fmt]
+    x = _probe_inputs(seed=2)
+    xt = torch.from_numpy(x).to(DEV)
+    scale = torch.ones(1, device=DEV)
+    codes, *_ = B.fp8_quantize(xt, fcode, jit=False, scale=scale)
+    got = codes.view(torch.int16).cpu().numpy().view(np.uint16) if fmt == "f16" else codes.cpu().numpy()
+    ref = encode(x, ofmt)
+    nan = np.isnan(x)
+    bad = np.nonzero(got[~nan].astype(np.int64) != ref[~nan].astype(np.int64))[0]
+    assert bad.size == 0, (bad.size, x[~nan][bad[:8]], got[~nan][bad[:8]], ref[~nan][bad[:8]])
+    assert np.all(np.isnan(decode(got[nan], ofmt)))
+
+
+@pytest.mark.parametrize("fmt", ["e4m3", "e5m2", "f16"])
+def test_dequantize_every_code(B, fmt):
+    fcode = {"e4m3": B.E4M3, "e5m2": B.E5M2, "f16": B.F16}[fmt]
+    ofmt = {"e4m3": E4M3, "e5m2": E5M2, "f16": FP16}[fmt]
+    n = 1 << ofmt.nbits
+    codes = np.arange(n, dtype=np.int64)
+    si = F32(0.0078125 * 3)
+    if fmt == "f16":
+        ct = torch.from_numpy(codes.astype(np.uint16).view(np.int16)).to(DEV).view(torch.float16)
+    else:
+        ct = torch.from_numpy(codes.astype(np.uint8)).to(DEV)
+    out = B.fp8_dequantize(ct, fcode, torch.tensor([si], device=DEV)).cpu().numpy()
+    ref = decode(codes, ofmt).astype(F32) * si
+    fin = np.isfinite(ref)
+    assert np.array_equal(out[fin], ref[fin])
+    assert np.array_equal(np.isnan(out), np.isnan(ref))
+
+
+def test_jit_quantize_single_tensor(B):
+    """fp8_quantize(jit): amax, scale = fl(448/amax), codes (App. B JIT)."""
+    rng = np.random.default_rng(4)
+    for n in (1, 15, 16, 17, 1000, 65536 + 7):
+        x = (rng.standard_t(3, size=n) * 1e-3).astype(F32)
+        codes, s, si, a, sat = B.fp8_quantize(torch.from_numpy(x).to(DEV), B.E4M3, jit=True, count_sat=True)
+        ref = OA.encode_scaled(x, E4M3, OA.E4M3_MAX, F32(np.abs(x).max()))
+        assert F32(a.item()) == ref.amax and F32(s.item()) == ref.scale and F32(si.item()) == ref.scale_inv
+        assert np.array_equal(codes.cpu().numpy(), ref.codes)
+        assert sat.item() == OP.sat_count(ref.codes)
+    # bf16 source: exact widening
+    xb = torch.from_numpy((rng.standard_normal(4097) * 3).astype(F32)).to(DEV).bfloat16()
+    codes, s, si, a, _ = B.fp8_quantize(xb, B.E4M3, jit=True)
+    xf = xb.float().cpu().numpy()
+    ref = OA.encode_scaled(xf, E4M3, OA.E4M3_MAX, F32(np.abs(xf).max()))
+    assert np.array_equal(codes.cpu().numpy(), ref.codes)
+
+
+# ----------------------------------------------------------------- the whole step
+RAGGED = [3, 16, 17, 64, 1000, 16384, 16385, 40000, 70001]
+
+
+def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float32,
+                     specials=None, amp=None, check_tensors=None):
+    """Run the device path for `steps` steps and the oracle on the same inputs; compare
+    every per-tensor output of every step.  check_tensors: oracle runs only on this
+    subset (valid because nothing couples two tensors except the skip flag, and the
+    inputs of a subset run are finite)."""
+    import synth
+    plan = B.Plan(numels, mode=mode, nranks=nranks)
+    w0 = plan.flat(torch.float32)
+    for t, v in enumerate(plan.views(w0)):
+        if v.numel():
+            synth.fill_weights(v, t)
+    dp = B.FP8DataParallel(plan, w0, lr=lr)
+    sub = list(range(plan.T)) if check_tensors is None else list(check_tensors)
+    ref_all = R.oracle_init(plan, w0)
+    ref_states = [ref_all[t] for t in sub]
+    mus = [F32(1.0)] * len(sub)
+    torch.cuda.synchronize()
+    for i, t in enumerate(sub):
+        R.assert_state_equal(R.state_np(B, plan, dp.state, t), ref_states[i], f"init t={t}")
+    for step in range(1, steps + 1):
+        grads = R.make_grads(plan, nranks, step, DEV, dtype,
+                             specials=(lambda f, r: specials(f, r, step)) if specials else None, amp=amp)
+        dp.step(grads if mode == B.MODE_SIMULATED else grads[0], lr=lr)
+        torch.cuda.synchronize()
+        gnp = [R.to_np_f32(g) for g in grads]
+        per_rank = [[g[plan.offsets[t]: plan.offsets[t] + plan.numels[t]] for t in sub] for g in gnp]
+        res = OS.train_step(per_rank, mus, ref_states, OA.hyper_params(lr, step))
+        assert bool(dp.skip.item()) == res["skip"], step
+        amax = dp.amax.cpu().numpy().reshape(-1, max(plan.T, 1))
+        s_g = dp.s_g.cpu().numpy()
+        g8 = dp.g8.cpu().numpy()
+        gs = dp.g_scale.cpu().numpy()
+        gsi = dp.g_scale_inv.cpu().numpy()
+        sat = dp.sat.cpu().numpy()
+        mu = dp.mu.cpu().numpy()
+        for i, t in enumerate(sub):
+            p = res["per_tensor"][i]
+            where = f"step {step} tensor {t} (n={plan.numels[t]})"
+            for r in range(amax.shape[0]):
+                a_ref = p["amax"][r]
+                assert (np.isnan(amax[r, t]) and np.isnan(a_ref)) or F32(amax[r, t]) == a_ref, where
+            assert F32(s_g[t]) == p["s_g"], (where, s_g[t], p["s_g"])
+            got = g8[plan.offsets[t]: plan.offsets[t] + plan.numels[t]]
+            if not p["skip"]:
+                bad = np.nonzero(got != p["codes"])[0]
+                assert bad.size == 0, f"{where}: {bad.size} reduced codes differ"
+                assert int(sat[t]) == p["sat"], (where, sat[t], p["sat"])
+            assert F32(gs[t]) == p["scale"], where
+            assert F32(gsi[t]) == p["scale_inv"], where
+            assert F32(mu[t]) == res["mu_next"][i], (where, mu[t], res["mu_next"][i])
+            R.assert_state_equal(R.state_np(B, plan, dp.state, t), res["states"][i], where)
+        mus = res["mu_next"]
+        ref_states = res["states"]
+    return plan, dp
+
+
+def test_local_ragged_multistep(B):
+    """N = 1 (LOCAL): 9 ragged tensors spanning tiles + tails, 6 steps with mu dynamics."""
+    _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=6)
+
+
+def test_local_bf16_gradients(B):
+    _run_and_compare(B, RAGGED[:6], B.MODE_LOCAL, 1, steps=2, dtype=torch.bfloat16)
+
+
+@pytest.mark.parametrize("N", [2, 3, 8])
+def test_simulated_ranks_multistep(B, N):
+    """N simulated ranks on one device (config C1 protocol): RS+AG degenerate to a local
+    rank-order sum; correlated heavy-tailed gradients overflow the sum so sat
+    and the mu halving path run."""
+    _run_and_compare(B, RAGGED, B.MODE_SIMULATED, N, steps=4)
+
+
+def test_edge_cases_empty_zero_and_tiny(B):
+    """Empty tensor, all-zero tensor (s_g -> 1), sub-min-subnormal tensor."""
+    numels = [0, 100, 33, 0, 5000, 77]
+    amp = [1.0, 0.0, 1e-30, 1.0, 1e-3, 1e-38]
+    _run_and_compare(B, numels, B.MODE_SIMULATED, 2, steps=2, amp=amp)
+
+
+def test_nonfinite_gradient_skips(B):
+    """inf on one rank / NaN on another: s_g = 0 -> skip, states unchanged, mu halves (R14)."""
+    def specials(flat, r, step):
+        if step == 2 and r == 1:
+            flat[5] = float("inf")
+        if step == 3 and r == 0:
+            flat[70000] = float("nan")
+    _run_and_compare(B, RAGGED, B.MODE_SIMULATED, 2, steps=4, specials=specials)
+
+
+def test_determinism(B):
+    numels = RAGGED
+    outs = []
+    for _ in range(2):
+        plan, dp = _run_and_compare(B, numels, B.MODE_SIMULATED, 2, steps=1)
+        outs.append((dp.g8.cpu().clone(), dp.state.master.data.cpu().clone(), dp.state.w8.data.cpu().clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a.view(torch.uint8) if a.dtype != torch.uint8 else a,
+                           b.view(torch.uint8) if b.dtype != torch.uint8 else b)
+
+
+def test_c1_full_size_two_simulated_ranks(B):
+    """Config C1 at full size (BASELINE.json configs[0]): one 4096x4096 fp32 gradient,
+    2 simulated ranks, one full step compared element by element."""
+    _run_and_compare(B, [4096 * 4096], B.MODE_SIMULATED, 2, steps=1)
+
+
+def test_c2_full_set_sampled_tensors(B):
+    """Config C2 (GPT-125M set, 147 tensors, 123.7M params) in the bench's launch
+    configuration; per-tensor independence lets the oracle check a subset
+    of tensors exactly: the 38.6M embedding, LayerNorms, biases, a 4d x d matrix, lnf."""
+    import synth
+    specs = synth.gpt_gradient_set("gpt-125m")
+    numels = [s.numel for s in specs]
+    pick = [0, 1, 2, 3, 4, 9, 10, len(specs) - 2, len(specs) - 1]
+    _run_and_compare(B, numels, B.MODE_LOCAL, 1, steps=2, check_tensors=pick)
