@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--lr", type=float, default=6e-4)   # GPT-125M max LR, Table 1
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true",
+                    help="profiling runs (ncu): no clock soak, no e2e, no cpu baseline")
     return ap.parse_args()
 
 
@@ -276,9 +278,9 @@ def main():
     torch.cuda.synchronize()
 
     # clock sampler runs through a ~1 s untimed soak and the timed region
-    sampler = ClockSampler(local)
+    sampler = None if args.quick else ClockSampler(local)
     t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < 1.0:
+    while sampler is not None and time.perf_counter() - t_soak < 1.0:
         dp.step(grads)
         torch.cuda.synchronize()
 
@@ -296,7 +298,7 @@ def main():
     barrier(world)
     B.prof_enable(False)
     prof = B.prof_read()
-    clocks = sampler.stop()
+    clocks = sampler.stop() if sampler is not None else None
     ms_local = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms_local, world)
 
@@ -327,7 +329,7 @@ def main():
 
     # ---------------- e2e: host gradients (pinned) -> device, step, results -> host
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.quick:
         host_g = torch.empty(grads.numel(), dtype=gdt, pin_memory=True)
         host_g.copy_(grads)
         out_h = torch.empty(3 * plan.T + 1, dtype=torch.float32, pin_memory=True)
@@ -353,7 +355,7 @@ def main():
                "d2h_bytes_per_step": out_h.numel() * 4}
 
     cpu = None
-    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+    if rank == 0 and N == 1 and not args.no_cpu_baseline and not args.quick:
         cpu = cpu_baseline(specs, args.config)
 
     if rank == 0:

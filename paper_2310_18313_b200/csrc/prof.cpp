@@ -65,8 +65,10 @@ extern "C" {
 
 int fp8lm_prof_enable(int on) {
   std::lock_guard<std::mutex> lk(g_mu);
-  for (auto& r : g_recs) { g_free.push_back(r.a); g_free.push_back(r.b); }
-  g_recs.clear();
+  if (on) {   // a new window: recycle the previous window's events
+    for (auto& r : g_recs) { g_free.push_back(r.a); g_free.push_back(r.b); }
+    g_recs.clear();
+  }
   g_on.store(on != 0);
   return FP8LM_OK;
 }
