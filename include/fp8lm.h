@@ -220,6 +220,15 @@ int fp8lm_prof_ids(void);
 int fp8lm_prof_read(int32_t id, const char** name, int64_t* launches, double* total_ms,
                     int32_t* is_ours);
 
+/* ----------------------------------------------------------- diagnostics (auxiliary) */
+/* Device self-test of the branch-free IEEE sqrt / division fast paths used by the
+ * AdamW kernels: every non-negative binary32 input for sqrt, `div_pairs` seeded
+ * pseudo-random (a, b) pairs for division, each compared bit-for-bit with
+ * __fsqrt_rn / __fdiv_rn wherever the fast path's range predicate accepts it.
+ * out4 (host): {sqrt mismatches, sqrt inputs accepted, div mismatches, div pairs
+ * accepted}.  Synchronous (allocates 32 bytes of device scratch; not a hot-path call). */
+int fp8lm_selftest_fastmath(uint64_t div_pairs, uint64_t seed, uint64_t* out4);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libfp8lm.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_2310_18313_b200.build` "
+        f"{LIB_PATH} is missing: build it with `python paper_2310_18313_b200/build.py` "
         "(or __graft_entry__.build()); there is no fallback path")
 
 lib = C.CDLL(LIB_PATH)
@@ -77,6 +77,7 @@ _sig("fp8lm_prof_enable", C.c_int, C.c_int)
 _sig("fp8lm_prof_ids", C.c_int)
 _sig("fp8lm_prof_read", C.c_int, _i32, C.POINTER(C.c_char_p), C.POINTER(_i64), C.POINTER(C.c_double),
      C.POINTER(_i32))
+_sig("fp8lm_selftest_fastmath", C.c_int, _u64, _u64, C.POINTER(_u64))
 _sig("fp8lm_state_init", C.c_int, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(STensors), C.POINTER(STensors), _p)
 
@@ -135,6 +136,13 @@ def zero_plan(numels: Sequence[int], nranks: int):
     load = (_i64 * nranks)()
     _check(lib.fp8lm_zero_plan(T, arr, nranks, owner, load), "fp8lm_zero_plan")
     return list(owner)[:T], list(load)
+
+
+def selftest_fastmath(div_pairs: int = 1 << 36, seed: int = 12345):
+    """-> dict(sqrt_bad, sqrt_accepted, div_bad, div_accepted) (see fp8lm.h)."""
+    out = (_u64 * 4)()
+    _check(lib.fp8lm_selftest_fastmath(div_pairs, seed, out), "fp8lm_selftest_fastmath")
+    return dict(sqrt_bad=out[0], sqrt_accepted=out[1], div_bad=out[2], div_accepted=out[3])
 
 
 def prof_enable(on: bool = True):

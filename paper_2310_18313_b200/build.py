@@ -1,6 +1,6 @@
 """Build libfp8lm.so in-tree with nvcc for sm_100a (no JIT, no torch extension cache).
 
-    python -m paper_2310_18313_b200.build          # or __graft_entry__.build()
+    python paper_2310_18313_b200/build.py [--force]     # or __graft_entry__.build()
 
 Flags: -gencode arch=compute_100a,code=sm_100a (arch-specific: the packed FP8 cvt and
 256-bit ld/st are sm_100a instructions); -fmad=false + IEEE div/sqrt so that every
