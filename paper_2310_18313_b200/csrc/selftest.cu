@@ -16,8 +16,8 @@ __global__ void k_check_sqrt(uint32_t lo, uint32_t hi, unsigned long long* bad,
   for (uint64_t b = (uint64_t)lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < hi;
        b += (uint64_t)gridDim.x * blockDim.x) {
     const float x = __uint_as_float((uint32_t)b);
-    bool ok;
-    const float f = sqrt_rn_fast(x, ok);
+    const bool ok = sqrt_chk(x) >= kSqrtChkMin && x < 1.2676506e30f;
+    const float f = sqrt_rn_core(x);
     if (ok) {
       ++na;
       const float r = __fsqrt_rn(x);
@@ -48,8 +48,9 @@ __global__ void k_check_div(uint64_t pairs, uint64_t seed, unsigned long long* b
     if ((i & 63u) == 0) { ma = (i & 64u) ? 0x7FFFFFu : 0u; mb = (i & 128u) ? 0x7FFFFFu : 1u; }
     const float a = __uint_as_float(((ra & 1u) << 31) | (ea << 23) | ma);
     const float b = __uint_as_float((eb << 23) | mb);
-    bool ok;
-    const float f = div_rn_fast(a, b, ok);
+    const bool ok = div_chk(a) >= kDivChkMin && fabsf(a) < 2.3058430e18f &&
+                    b >= 8.6736174e-19f && b < 2.3058430e18f;          // 2^-60 .. 2^61
+    const float f = div_rn_core(a, b);
     if (ok) {
       ++na;
       const float r = __fdiv_rn(a, b);
