@@ -66,7 +66,7 @@ namespace fp8lm {
 // durations per name.  Used by bench.py for the per-kernel roofline and launch count.
 enum ProfId : int {
   P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
-  P_ADAM_FINALIZE, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
+  P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
   P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_COUNT
 };
 bool prof_on();

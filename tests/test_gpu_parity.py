@@ -205,3 +205,15 @@ def test_c2_full_set_sampled_tensors(B):
     numels = [s.numel for s in specs]
     pick = [0, 1, 2, 3, 4, 9, 10, len(specs) - 2, len(specs) - 1]
     _run_and_compare(B, numels, B.MODE_LOCAL, 1, steps=2, check_tensors=pick)
+
+
+def test_amax_screen_fallback_large_lr(B):
+    """lr = 0.05 moves the largest weights by far more than the 2^-6 screen margin, so
+    pass 1's certified amax(w') screen fails for most tensors and k_adam_wfix
+    recomputes them exactly; results must still be bit-exact."""
+    _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=3, lr=0.05)
+
+
+def test_amax_screen_mixed_simulated(B):
+    """Moderate lr: some tensors pass the screen, some fall back."""
+    _run_and_compare(B, RAGGED, B.MODE_SIMULATED, 2, steps=3, lr=2e-3)
