@@ -229,6 +229,8 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
   p->off_acc_amax = take(sizeof(uint32_t) * std::max(nsim * T, 1));
   p->off_acc_state = take(sizeof(uint32_t) * std::max(3 * T, 1));
   p->off_sat_part = take(sizeof(uint32_t) * std::max(T, 1));
+  p->off_sat_acc = take(sizeof(uint32_t) * std::max(T, 1));
+  p->off_ctr = take(sizeof(uint32_t) * 4);
   p->off_acc_end = off;
   if (mode == FP8LM_MODE_NCCL) {
     p->off_send = take((size_t)(p->shard * nranks));
@@ -272,7 +274,7 @@ int fp8lm_plan_bind(fp8lm_plan* p, void* ws, size_t ws_bytes, void* stream) {
   CUDA_TRY(cudaMemcpyAsync(b + p->off_item_start, p->item_start.data(), sizeof(int64_t) * (p->T + 1), cudaMemcpyHostToDevice, s));
   if (!p->shard_items.empty())
     CUDA_TRY(cudaMemcpyAsync(b + p->off_shard_items, p->shard_items.data(), sizeof(ShardItem) * p->shard_items.size(), cudaMemcpyHostToDevice, s));
-  // accumulators (acc_amax, acc_state, sat_part: consecutive regions) must be zero at rest
+  // accumulators (acc_amax, acc_state, sat_part, sat_acc, counters: consecutive) zero at rest
   CUDA_TRY(cudaMemsetAsync(b + p->off_acc_amax, 0, p->off_acc_end - p->off_acc_amax, s));
   CUDA_TRY(cudaStreamSynchronize(s));   // host tables are pageable: finish before returning
   DevPlan& d = p->dev;
@@ -291,6 +293,8 @@ int fp8lm_plan_bind(fp8lm_plan* p, void* ws, size_t ws_bytes, void* stream) {
   d.send = p->mode == FP8LM_MODE_NCCL ? b + p->off_send : nullptr;
   d.recv = p->mode == FP8LM_MODE_NCCL ? b + p->off_recv : nullptr;
   d.sim_codes = p->mode == FP8LM_MODE_SIMULATED ? b + p->off_sim : nullptr;
+  d.sat_acc = reinterpret_cast<uint32_t*>(b + p->off_sat_acc);
+  d.counters = reinterpret_cast<uint32_t*>(b + p->off_ctr);
   p->ws = ws;
   p->bound = true;
   return FP8LM_OK;
@@ -368,14 +372,13 @@ int fp8lm_amax_scale_sync(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, in
   if (p->T > 0 && (rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "amax_scale_sync"))) return rc;
   if (!mu || !amax_out || !s_g || !skip) return fail(FP8LM_EINVAL, "amax_scale_sync: NULL output");
   cudaStream_t s = S(stream);
-  {
-    ProfScope ps_(P_MEMSET, s);
+  if (p->T == 0) {
     CUDA_TRY(cudaMemsetAsync(skip, 0, sizeof(int32_t), s));
+    return FP8LM_OK;
   }
-  if (p->T == 0) return FP8LM_OK;
-  CUDA_TRY(launch_amax(p->dev, srcs, nsrc, src_dtype, s));
   const bool nccl = p->mode == FP8LM_MODE_NCCL;
-  CUDA_TRY(launch_scale(p->dev, nsrc, mu, amax_out, s_g, skip, !nccl, s));
+  // A1 amax; its last CTA computes the scales (A2) and, without an exchange, s_g + skip
+  CUDA_TRY(launch_amax(p->dev, srcs, nsrc, src_dtype, mu, amax_out, s_g, skip, !nccl, s));
   if (nccl) {
 #ifdef FP8LM_WITH_NCCL
     // Eq. 4: s'_g = min(s'_1, ..., s'_N) — T floats over NVLink
@@ -406,20 +409,18 @@ int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int
     return fail(FP8LM_EINVAL, "grad_allreduce: g8 NULL or not 256-byte aligned");
   cudaStream_t s = S(stream);
   if (p->T == 0) return FP8LM_OK;
-  {
-    ProfScope ps_(P_MEMSET, s);
-    CUDA_TRY(cudaMemsetAsync(sat, 0, sizeof(uint32_t) * p->T, s));
-  }
   const DevPlan& d = p->dev;
+  const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
   if (p->mode == FP8LM_MODE_LOCAL) {
-    // N = 1: the reduce-scatter / all-gather are the identity (A4, A5); count here
+    // N = 1: the reduce-scatter / all-gather are the identity (A4, A5); quantize counts
+    // saturation and its last CTA runs the Eq. 6 / mu tail
     uint8_t* dst[1] = {g8};
-    CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, sat, s));
+    CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, &tail, s));
   } else if (p->mode == FP8LM_MODE_SIMULATED) {
     uint8_t* dst[FP8LM_MAX_SIM_RANKS];
     for (int r = 0; r < nsrc; ++r) dst[r] = d.sim_codes + (int64_t)r * p->total;
     CUDA_TRY(launch_quantize(d, srcs, dst, nsrc, src_dtype, s_g, nullptr, s));
-    CUDA_TRY(launch_reduce(d, d.sim_codes, p->total, nsrc, 0, false, g8, sat, s));
+    CUDA_TRY(launch_reduce(d, d.sim_codes, p->total, nsrc, 0, false, g8, s_g, &tail, s));
   } else {
 #ifdef FP8LM_WITH_NCCL
     const int64_t S_ = p->shard;
@@ -430,11 +431,9 @@ int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int
       ProfScope ps_(P_NCCL_A2A, s);
       NCCL_TRY(ncclAlltoAll(d.send, d.recv, (size_t)S_, ncclUint8, comm->comm, s));
     }
-    {
-      ProfScope ps_(P_MEMSET, s);
-      CUDA_TRY(cudaMemsetAsync(d.sat_part, 0, sizeof(uint32_t) * p->T, s));
-    }
-    CUDA_TRY(launch_reduce(d, d.recv, S_, p->nranks, S_ * p->rank, true, g8, d.sat_part, s));
+    // own shard: rank-order FP32 sum, requantize, per-shard saturation counts (sat_part
+    // was zeroed by this step's amax epilogue)
+    CUDA_TRY(launch_reduce(d, d.recv, S_, p->nranks, S_ * p->rank, true, g8, s_g, nullptr, s));
     // all-gather of the reduced shards (in place) + global saturation counts
     {
       ProfScope ps_(P_NCCL_AG_SUM, s);
@@ -443,11 +442,11 @@ int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int
       NCCL_TRY(ncclAllReduce(d.sat_part, sat, (size_t)p->T, ncclUint32, ncclSum, comm->comm, s));
       NCCL_TRY(ncclGroupEnd());
     }
+    CUDA_TRY(launch_allreduce_finalize(d, s_g, tail, s));
 #else
     return fail(FP8LM_EUNSUPPORTED, "built without NCCL");
 #endif
   }
-  CUDA_TRY(launch_allreduce_finalize(d, p->nranks, s_g, skip, sat, g_scale, g_scale_inv, mu, s));
   return FP8LM_OK;
 }
 

@@ -36,6 +36,20 @@ struct DevPlan {
   uint8_t* send;            // [N*S]     NCCL send buffer (quantized codes, flat)
   uint8_t* recv;            // [N*S]     NCCL all-to-all receive buffer
   uint8_t* sim_codes;       // [nsim*total] simulated ranks' quantized codes
+  uint32_t* sat_acc;        // [T]       saturation counts of the step (zero at rest)
+  uint32_t* counters;       // [4]       grid_last_block tickets (zero at rest)
+};
+
+constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2;
+
+// outputs of the Eq. 6 / mu tail of fp8lm_grad_allreduce
+struct TailArgs {
+  int nranks;
+  const int32_t* skip;
+  uint32_t* sat;
+  float* g_scale;
+  float* g_scale_inv;
+  float* mu;
 };
 
 }  // namespace fp8lm
@@ -52,7 +66,8 @@ struct fp8lm_plan {
   int64_t g8_bytes = 0;
   // workspace layout (byte offsets)
   size_t off_numel = 0, off_offset = 0, off_item_start = 0, off_shard_items = 0;
-  size_t off_acc_amax = 0, off_acc_state = 0, off_sat_part = 0, off_acc_end = 0;
+  size_t off_acc_amax = 0, off_acc_state = 0, off_sat_part = 0, off_sat_acc = 0, off_ctr = 0,
+         off_acc_end = 0;
   size_t off_send = 0, off_recv = 0, off_sim = 0, ws_bytes = 0;
   void* ws = nullptr;
   fp8lm::DevPlan dev{};
@@ -80,19 +95,17 @@ struct ProfScope {
 
 // kernel launchers (kernels.cu); return cudaError_t of the launch
 cudaError_t launch_amax(const DevPlan& p, const void* const* srcs, int nsrc, int src_dtype,
-                        cudaStream_t s);
-cudaError_t launch_scale(const DevPlan& p, int nsrc, const float* mu, float* amax_out,
-                         float* s_out, int32_t* skip, bool finalize, cudaStream_t s);
+                        const float* mu, float* amax_out, float* s_out, int32_t* skip,
+                        bool finalize, cudaStream_t s);
 cudaError_t launch_scale_fix(const DevPlan& p, float* s_g, int32_t* skip, cudaStream_t s);
 cudaError_t launch_quantize(const DevPlan& p, const void* const* srcs, uint8_t* const* dsts,
-                            int nsrc, int src_dtype, const float* s_g, uint32_t* sat,
+                            int nsrc, int src_dtype, const float* s_g, const TailArgs* tail,
                             cudaStream_t s);
 cudaError_t launch_reduce(const DevPlan& p, const uint8_t* base, int64_t stride, int nsrc,
-                          int64_t shift, bool shard_items, uint8_t* dst, uint32_t* sat,
-                          cudaStream_t s);
-cudaError_t launch_allreduce_finalize(const DevPlan& p, int nranks, const float* s_g,
-                                      const int32_t* skip, const uint32_t* sat, float* g_scale,
-                                      float* g_scale_inv, float* mu, cudaStream_t s);
+                          int64_t shift, bool shard_items, uint8_t* dst, const float* s_g,
+                          const TailArgs* tail, cudaStream_t s);
+cudaError_t launch_allreduce_finalize(const DevPlan& p, const float* s_g, const TailArgs& tail,
+                                      cudaStream_t s);
 cudaError_t launch_adam(const DevPlan& p, const uint8_t* g8, const float* g_sinv,
                         const fp8lm_stensors& m1, const fp8lm_stensors& v,
                         const fp8lm_stensors& w, const fp8lm_stensors& w8,
