@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--lr", type=float, default=6e-4)   # GPT-125M max LR, Table 1
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--grad-sets", type=int, default=0,
+                    help="independent gradient sets rotated step by step (0: 4 for GPT-125M, "
+                         "2 otherwise); a fixed gradient would drive every weight the same way")
     ap.add_argument("--quick", action="store_true",
                     help="profiling runs (ncu): no clock soak, no e2e, no cpu baseline")
     return ap.parse_args()
@@ -266,22 +269,32 @@ def main():
     w0 = plan.flat(torch.float32)
     for t, v in enumerate(plan.views(w0)):
         synth.fill_weights(v, t)
-    grads = plan.flat(gdt)
-    for t, v in enumerate(plan.views(grads)):
-        synth.fill_gradient(v, 1, t, rank)
+    R = args.grad_sets or (4 if args.config == "gpt-125m" else 2)
+    gsets = []
+    for r_ in range(R):
+        g = plan.flat(gdt)
+        for t, v in enumerate(plan.views(g)):
+            synth.fill_gradient(v, 1 + r_, t, rank)
+        gsets.append(g)
+    grads = gsets[0]
     dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr)
     del w0
     torch.cuda.synchronize()
+    nstep = [0]
+
+    def step():
+        dp.step(gsets[nstep[0] % R])
+        nstep[0] += 1
 
     for _ in range(args.warmup):
-        dp.step(grads)
+        step()
     torch.cuda.synchronize()
 
     # clock sampler runs through a ~1 s untimed soak and the timed region
     sampler = None if args.quick else ClockSampler(local)
     t_soak = time.perf_counter()
     while sampler is not None and time.perf_counter() - t_soak < 1.0:
-        dp.step(grads)
+        step()
         torch.cuda.synchronize()
 
     # ---------------- timed region: K steps, per-launch CUDA events on the launch stream
@@ -292,7 +305,7 @@ def main():
     B.prof_enable(True)
     ev0.record(stream)
     for _ in range(args.steps):
-        dp.step(grads)
+        step()
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
@@ -330,12 +343,19 @@ def main():
     # ---------------- e2e: host gradients (pinned) -> device, step, results -> host
     e2e = None
     if not args.no_e2e and not args.quick:
-        host_g = torch.empty(grads.numel(), dtype=gdt, pin_memory=True)
-        host_g.copy_(grads)
+        host_sets = []
+        for g in gsets:
+            h = torch.empty(g.numel(), dtype=gdt, pin_memory=True)
+            h.copy_(g)
+            host_sets.append(h)
+        host_g = host_sets[0]
         out_h = torch.empty(3 * plan.T + 1, dtype=torch.float32, pin_memory=True)
         out_d = torch.empty(3 * plan.T + 1, dtype=torch.float32, device="cuda")
+        ne = [0]
+
         def e2e_step():
-            grads.copy_(host_g, non_blocking=True)
+            grads.copy_(host_sets[ne[0] % R], non_blocking=True)
+            ne[0] += 1
             dp.step(grads)
             torch.cat([dp.mu, dp.s_g, dp.sat.float(), dp.skip.float()], out=out_d)
             out_h.copy_(out_d, non_blocking=True)
@@ -369,6 +389,7 @@ def main():
                        "alg_bytes_per_param_per_rank": bytes_rank / params,
                        "parallelism": f"dp{N}" if N > 1 else "single", "state_scaling": "jit",
                        "l2": "inputs larger than L2 (step moves %.2f GB/rank > 126 MB)" % (bytes_rank / 1e9),
+                       "grad_sets_rotated": R,
                        "hbm_frac_of_8tbs": value / N / 8000.0},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "kernels": breakdown,
