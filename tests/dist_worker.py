@@ -1,0 +1,111 @@
+"""torchrun worker for the multi-GPU parity test (tests/test_gpu_nccl.py).
+
+Each rank runs the NCCL-mode hot path (fp8lm_amax_scale_sync -> fp8lm_grad_allreduce
+[all-to-all, rank-order reduce, all-gather] -> fp8lm_adam_step) on its own synthetic
+gradients, regenerates every other rank's gradients locally (synth is deterministic),
+runs the N-rank CPU oracle and compares its own outputs element by element.  Exit code 0
+iff every rank matched bit-exactly.
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+        tests/dist_worker.py [--steps 3]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+from oracle import adam as OA  # noqa: E402
+from oracle import step as OS  # noqa: E402
+from tests import _gpu_ref as R  # noqa: E402
+
+F32 = np.float32
+NUMELS = [3, 16, 17, 64, 1000, 16384, 16385, 40000, 70001, 5]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--lr", type=float, default=3e-4)
+    args = ap.parse_args()
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, N = dist.get_rank(), dist.get_world_size()
+    import paper_2310_18313_b200 as B
+
+    comm = B.Comm.from_torch_distributed()
+    plan = B.Plan(NUMELS, mode=B.MODE_NCCL, nranks=N, rank=rank)
+    w0 = plan.flat(torch.float32)
+    for t, v in enumerate(plan.views(w0)):
+        synth.fill_weights(v, t)
+    dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr)
+    ref_states = R.oracle_init(plan, w0)
+    mus = [F32(1.0)] * plan.T
+    ok = True
+    msgs = []
+    for step in range(1, args.steps + 1):
+        # every rank's gradient, generated here (rank r's own buffer is the input)
+        all_grads = []
+        for r in range(N):
+            flat = plan.flat(torch.float32)
+            for t, v in enumerate(plan.views(flat)):
+                synth.fill_gradient(v, step, t, r)
+            if step == 2 and r == N - 1:
+                flat[plan.offsets[4] + 7] = 3.0e5      # one huge value: sum saturates, mu halves
+            all_grads.append(flat)
+        dp.step(all_grads[rank], lr=args.lr)
+        torch.cuda.synchronize()
+        gnp = [R.to_np_f32(g) for g in all_grads]
+        per_rank = [[g[plan.offsets[t]: plan.offsets[t] + plan.numels[t]] for t in range(plan.T)]
+                    for g in gnp]
+        res = OS.train_step(per_rank, mus, ref_states, OA.hyper_params(args.lr, step))
+        g8 = dp.g8.cpu().numpy()
+        s_g = dp.s_g.cpu().numpy()
+        sat = dp.sat.cpu().numpy()
+        mu = dp.mu.cpu().numpy()
+        gs = dp.g_scale.cpu().numpy()
+        if bool(dp.skip.item()) != res["skip"]:
+            ok = False
+            msgs.append(f"step {step}: skip differs")
+        for t in range(plan.T):
+            p = res["per_tensor"][t]
+            sl = slice(plan.offsets[t], plan.offsets[t] + plan.numels[t])
+            checks = [
+                ("codes", np.array_equal(g8[sl], p["codes"])),
+                ("s_g", F32(s_g[t]) == p["s_g"]),
+                ("sat", int(sat[t]) == p["sat"]),
+                ("scale", F32(gs[t]) == p["scale"]),
+                ("mu", F32(mu[t]) == res["mu_next"][t]),
+            ]
+            for name, good in checks:
+                if not good:
+                    ok = False
+                    msgs.append(f"rank {rank} step {step} tensor {t}: {name} differs")
+            try:
+                R.assert_state_equal(R.state_np(B, plan, dp.state, t), res["states"][t],
+                                     f"rank {rank} step {step} tensor {t}")
+            except AssertionError as e:
+                ok = False
+                msgs.append(str(e)[:300])
+        mus = res["mu_next"]
+        ref_states = res["states"]
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    for m in msgs[:10]:
+        print(m, flush=True)
+    if rank == 0:
+        print(f"NCCL parity N={N}: {'OK' if flag.item() == 1 else 'MISMATCH'}", flush=True)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,46 @@
+"""Multi-GPU parity of the NCCL mode (one process per GPU, torchrun), bit-exact against
+the N-rank oracle: amax -> MIN all-reduce of the scales -> E4M3 quantize -> all-to-all
+-> rank-order FP32 reduce of the own shard -> in-place all-gather + summed saturation
+counts -> mu -> FP8 AdamW.  Needs >= 2 GPUs (gpurun --gpus 2 / 4)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from tests.conftest import gpu_available
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available() or _ngpus() < 2, reason="needs >= 2 GPUs")]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_nccl_mode_bit_exact(n):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "dist_worker.py"), "--steps", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert f"NCCL parity N={n}: OK" in r.stdout
