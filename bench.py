@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="gpt-125m", choices=["gpt-125m", "gpt-7b", "gpt-13b"])
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"], help="gradient dtype")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: fused peer-memory reduce-scatter/all-gather kernel (p2p) or "
+                         "NCCL all-to-all + all-gather around the reduce kernel (nccl)")
     ap.add_argument("--lr", type=float, default=6e-4)   # GPT-125M max LR, Table 1
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -263,7 +266,7 @@ def main():
     params = sum(numels)
     N = world
     comm = B.Comm.from_torch_distributed() if N > 1 else None
-    mode = B.MODE_NCCL if N > 1 else B.MODE_LOCAL
+    mode = (B.MODE_P2P if args.exchange == "p2p" else B.MODE_NCCL) if N > 1 else B.MODE_LOCAL
     plan = B.Plan(numels, mode=mode, nranks=N, rank=rank)
     gdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     w0 = plan.flat(torch.float32)
@@ -388,6 +391,7 @@ def main():
                        "tensors": plan.T, "params": params, "grad_dtype": args.dtype,
                        "alg_bytes_per_param_per_rank": bytes_rank / params,
                        "parallelism": f"dp{N}" if N > 1 else "single", "state_scaling": "jit",
+                       "exchange": (args.exchange if N > 1 else "none"),
                        "l2": "inputs larger than L2 (step moves %.2f GB/rank > 126 MB)" % (bytes_rank / 1e9),
                        "grad_sets_rotated": R,
                        "hbm_frac_of_8tbs": value / N / 8000.0},

@@ -67,8 +67,13 @@ typedef enum {
   FP8LM_MODE_LOCAL = 0,      /* nranks must be 1: one process, one GPU, no exchange     */
   FP8LM_MODE_SIMULATED = 1,  /* nranks simulated ranks whose gradients all live on this
                                 device (config C1); the exchange is a local read       */
-  FP8LM_MODE_NCCL = 2        /* one process per GPU; exchange over NCCL (NVLink)       */
+  FP8LM_MODE_NCCL = 2,       /* one process per GPU; exchange over NCCL (NVLink)       */
+  FP8LM_MODE_P2P = 3         /* one process per GPU; the exchange runs inside this
+                                library's kernels over NVLink peer memory (CUDA IPC
+                                windows of fp8lm_peer_setup); NCCL only bootstraps      */
 } fp8lm_mode;
+
+#define FP8LM_MAX_P2P_RANKS 8     /* ranks of one NVLink / NVSwitch domain in mode P2P */
 
 typedef struct fp8lm_plan fp8lm_plan;   /* opaque */
 typedef struct fp8lm_comm fp8lm_comm;   /* opaque: owns an ncclComm_t */
@@ -141,6 +146,18 @@ size_t fp8lm_plan_workspace_bytes(const fp8lm_plan* plan);
  * EWORKSPACE if ws is NULL / too small / misaligned. */
 int fp8lm_plan_bind(fp8lm_plan* plan, void* ws, size_t ws_bytes, void* stream);
 
+/* Mode P2P, collective (every rank, after fp8lm_plan_bind): allocate this rank's
+ * symmetric windows — the quantized send buffer (N*S bytes), the reduced-code buffer
+ * g8 (N*S bytes) and a small signal / exchange pad — exchange their CUDA IPC handles over
+ * `comm` (ncclAllGather) and map every peer's windows.  The windows are owned by the
+ * plan (freed by fp8lm_plan_destroy): the one exception to "the caller owns all memory".
+ * Synchronous.  EINVAL unless mode == P2P and comm matches the plan; ECUDA / ENCCL on
+ * failure. */
+int fp8lm_peer_setup(fp8lm_plan* plan, fp8lm_comm* comm, void* stream);
+/* Mode P2P: this rank's g8 window (device); pass it as g8 to the calls below.  NULL if
+ * fp8lm_peer_setup has not run. */
+uint8_t* fp8lm_peer_g8(const fp8lm_plan* plan);
+
 /* ------------------------------------------- (1) fp8_quantize: one scaling tensor */
 /* App. B JIT scaling + App. A encode.  src: n elements of src_dtype (F32 or BF16),
  * any alignment.  fmt: E4M3 or E5M2 (codes to dst, uint8[n]) or F16 (uint16[n]).
@@ -165,7 +182,9 @@ int fp8lm_dequantize(const void* codes, int32_t fmt, int64_t n, const float* sca
  *   s_r[t]    = fl(fl(448 / amax_r[t]) * mu[t])   (0 if non-finite, +inf if amax == 0)
  *   s_g[t]    = min_r s_r[t]  (Eq. 4; NCCL: ncclAllReduce MIN over `comm`)
  *   s_g == 0 -> *skip = 1;  s_g == +inf -> s_g = 1.         -> s_g [T], skip [1]
- * mu [T] is read only.  comm must be non-NULL iff mode == NCCL. */
+ * mu [T] is read only.  comm must be non-NULL iff mode == NCCL.  Mode P2P: the MIN over
+ * ranks is exchanged through the peers' pads by the amax kernel's last CTA (comm unused,
+ * may be NULL). */
 int fp8lm_amax_scale_sync(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
                           int32_t src_dtype, const float* mu, float* amax_out,
                           float* s_g, int32_t* skip, void* stream);
@@ -178,7 +197,10 @@ int fp8lm_amax_scale_sync(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
  * sat[t]     = #{i : |decode(g8[t][i])| == 448}  ("attains the maximum", R4)
  * mu[t]     <- mu_next: halve if *skip or sat*1e5 > numel[t], else min(2, fl(mu*2^(1/1000)))
  *              (R1-R3) — updated in place for the next step.
- * grads as in (2).  g8: fp8lm_plan_g8_bytes bytes.  All outputs are device arrays [T]. */
+ * grads as in (2).  g8: fp8lm_plan_g8_bytes bytes.  All outputs are device arrays [T].
+ * Mode P2P: g8 must be fp8lm_peer_g8(plan); one kernel reads every rank's quantized
+ * shard over NVLink, reduces in rank order and stores the result into every rank's g8
+ * (reduce-scatter + all-gather fused), with sys-scope flag barriers in the peers' pads. */
 int fp8lm_grad_allreduce(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
                          int32_t src_dtype, const float* s_g, const int32_t* skip,
                          uint8_t* g8, float* g_scale, float* g_scale_inv, uint32_t* sat,

@@ -26,7 +26,7 @@ lib = C.CDLL(LIB_PATH)
 # ------------------------------------------------------------------ constants (fp8lm.h)
 OK, EINVAL, ECUDA, ENCCL, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 E4M3, E5M2, F16, BF16, F32 = 0, 1, 2, 3, 4
-MODE_LOCAL, MODE_SIMULATED, MODE_NCCL = 0, 1, 2
+MODE_LOCAL, MODE_SIMULATED, MODE_NCCL, MODE_P2P = 0, 1, 2, 3
 ALIGN_ELEMS = 64
 MAX_SIM_RANKS = 16
 
@@ -67,6 +67,8 @@ _sig("fp8lm_plan_shard_bytes", _i64, _p)
 _sig("fp8lm_plan_shard_begin", _i64, _p, _i32)
 _sig("fp8lm_plan_workspace_bytes", C.c_size_t, _p)
 _sig("fp8lm_plan_bind", C.c_int, _p, _p, C.c_size_t, _p)
+_sig("fp8lm_peer_setup", C.c_int, _p, _p, _p)
+_sig("fp8lm_peer_g8", _p, _p)
 _sig("fp8lm_quantize", C.c_int, _p, _i32, _i64, _i32, _p, _p, _p, _p, _i32, _p, _p)
 _sig("fp8lm_dequantize", C.c_int, _p, _i32, _i64, _p, _p, _p)
 _sig("fp8lm_amax_scale_sync", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p)
@@ -221,6 +223,21 @@ class Plan:
             lib.fp8lm_plan_destroy(h)
             self.handle = None
 
+    def peer_setup(self, comm: "Comm", stream=None):
+        """Mode P2P: map every rank's windows (collective; see fp8lm_peer_setup)."""
+        _check(lib.fp8lm_peer_setup(self.handle, comm.handle, _stream(stream)), "fp8lm_peer_setup")
+
+    def peer_g8(self) -> torch.Tensor:
+        """Mode P2P: this rank's g8 window as a uint8 tensor (no copy)."""
+        ptr = lib.fp8lm_peer_g8(self.handle)
+        if not ptr:
+            raise FP8LMError("peer_g8: fp8lm_peer_setup has not run")
+
+        class _Win:
+            __cuda_array_interface__ = {"shape": (self.g8_bytes,), "typestr": "|u1",
+                                        "data": (ptr, False), "version": 3}
+        return torch.as_tensor(_Win(), device=self.device)
+
     def shard_begin(self, rank: int) -> int:
         return lib.fp8lm_plan_shard_begin(self.handle, rank)
 
@@ -356,7 +373,12 @@ class FP8DataParallel:
         self.amax = torch.zeros(nsim * T, dtype=torch.float32, device=dev)
         self.s_g = torch.zeros(T, dtype=torch.float32, device=dev)
         self.skip = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.g8 = plan.flat(torch.uint8, nbytes_like_g8=True)
+        if plan.mode == MODE_P2P:
+            plan.peer_setup(comm)
+            self.g8 = plan.peer_g8()
+            self.comm = None            # the exchange runs in the library's kernels
+        else:
+            self.g8 = plan.flat(torch.uint8, nbytes_like_g8=True)
         self.g_scale = torch.zeros(T, dtype=torch.float32, device=dev)
         self.g_scale_inv = torch.zeros(T, dtype=torch.float32, device=dev)
         self.sat = torch.zeros(T, dtype=torch.int32, device=dev)

@@ -174,15 +174,18 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
                       int32_t rank, fp8lm_plan** out) {
   if (!out) return fail(FP8LM_EINVAL, "plan_create: out is NULL");
   if (T < 0 || (T > 0 && !numels)) return fail(FP8LM_EINVAL, "plan_create: bad T / numels");
-  if (mode < FP8LM_MODE_LOCAL || mode > FP8LM_MODE_NCCL)
+  if (mode < FP8LM_MODE_LOCAL || mode > FP8LM_MODE_P2P)
     return fail(FP8LM_EINVAL, "plan_create: bad mode %d", mode);
   if (nranks < 1) return fail(FP8LM_EINVAL, "plan_create: nranks must be >= 1");
   if (mode == FP8LM_MODE_LOCAL && nranks != 1)
     return fail(FP8LM_EINVAL, "plan_create: mode LOCAL needs nranks == 1");
   if (mode == FP8LM_MODE_SIMULATED && nranks > FP8LM_MAX_SIM_RANKS)
     return fail(FP8LM_EINVAL, "plan_create: at most %d simulated ranks", FP8LM_MAX_SIM_RANKS);
-  if (mode == FP8LM_MODE_NCCL && (rank < 0 || rank >= nranks))
+  const bool dist = mode == FP8LM_MODE_NCCL || mode == FP8LM_MODE_P2P;
+  if (dist && (rank < 0 || rank >= nranks))
     return fail(FP8LM_EINVAL, "plan_create: rank %d out of range", rank);
+  if (mode == FP8LM_MODE_P2P && nranks > FP8LM_MAX_P2P_RANKS)
+    return fail(FP8LM_EINVAL, "plan_create: mode P2P supports at most %d ranks", FP8LM_MAX_P2P_RANKS);
   for (int t = 0; t < T; ++t)
     if (numels[t] < 0) return fail(FP8LM_EINVAL, "plan_create: numel[%d] < 0", t);
 
@@ -190,7 +193,7 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
   p->T = T;
   p->mode = mode;
   p->nranks = nranks;
-  p->rank = mode == FP8LM_MODE_NCCL ? rank : 0;
+  p->rank = dist ? rank : 0;
   p->numel.assign(numels, numels + T);
   p->offset.resize(T);
   p->item_start.resize(T + 1);
@@ -204,7 +207,7 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
   p->item_start[T] = items;
   p->total = run;
   p->g8_bytes = run;
-  if (mode == FP8LM_MODE_NCCL) {
+  if (dist) {
     // reduce-scatter shards: N contiguous byte ranges of the flat code buffer, each a
     // multiple of 64 bytes so that every shard item starts 16-byte aligned
     const int64_t N = nranks;
@@ -243,9 +246,78 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
 }
 
 int fp8lm_plan_destroy(fp8lm_plan* plan) {
+  if (!plan) return FP8LM_OK;
+  for (void* m : plan->mapped) cudaIpcCloseMemHandle(m);
+  if (plan->win_send) cudaFree(plan->win_send);
+  if (plan->win_g8) cudaFree(plan->win_g8);
+  if (plan->win_pad) cudaFree(plan->win_pad);
   delete plan;
   return FP8LM_OK;
 }
+
+// ---------------------------------------------------------------- mode P2P windows
+int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
+  if (!p || p->mode != FP8LM_MODE_P2P) return fail(FP8LM_EINVAL, "peer_setup: plan mode is not P2P");
+  if (!p->bound) return fail(FP8LM_EWORKSPACE, "peer_setup: plan not bound");
+  if (p->p2p_ready) return FP8LM_OK;
+#ifdef FP8LM_WITH_NCCL
+  if (!comm || comm->nranks != p->nranks || comm->rank != p->rank)
+    return fail(FP8LM_EINVAL, "peer_setup: communicator does not match the plan");
+  const int N = p->nranks;
+  const size_t win = (size_t)p->g8_bytes;
+  p->pad_bytes = kPadData + (size_t)N * std::max(p->T, 1) * (sizeof(float) + sizeof(uint32_t));
+  CUDA_TRY(cudaMalloc(&p->win_send, win));
+  CUDA_TRY(cudaMalloc(&p->win_g8, win));
+  CUDA_TRY(cudaMalloc(&p->win_pad, p->pad_bytes));
+  CUDA_TRY(cudaMemset(p->win_pad, 0, p->pad_bytes));
+  CUDA_TRY(cudaMemset(p->win_send, 0, win));
+  struct Handles { cudaIpcMemHandle_t send, g8, pad; };
+  Handles mine;
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.send, p->win_send));
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.g8, p->win_g8));
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.pad, p->win_pad));
+  Handles* dev = nullptr;
+  CUDA_TRY(cudaMalloc(&dev, sizeof(Handles) * N));
+  CUDA_TRY(cudaMemcpy(dev + p->rank, &mine, sizeof(Handles), cudaMemcpyHostToDevice));
+  cudaStream_t s = S(stream);
+  NCCL_TRY(ncclAllGather(dev + p->rank, dev, sizeof(Handles), ncclUint8, comm->comm, s));
+  std::vector<Handles> all(N);
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaMemcpy(all.data(), dev, sizeof(Handles) * N, cudaMemcpyDeviceToHost));
+  cudaFree(dev);
+  PeerTable tab{};
+  for (int q = 0; q < N; ++q) {
+    if (q == p->rank) {
+      tab.send[q] = p->win_send;
+      tab.g8[q] = p->win_g8;
+      tab.pad[q] = p->win_pad;
+      continue;
+    }
+    void *ps = nullptr, *pg = nullptr, *pp = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&ps, all[q].send, cudaIpcMemLazyEnablePeerAccess));
+    p->mapped.push_back(ps);
+    CUDA_TRY(cudaIpcOpenMemHandle(&pg, all[q].g8, cudaIpcMemLazyEnablePeerAccess));
+    p->mapped.push_back(pg);
+    CUDA_TRY(cudaIpcOpenMemHandle(&pp, all[q].pad, cudaIpcMemLazyEnablePeerAccess));
+    p->mapped.push_back(pp);
+    tab.send[q] = static_cast<uint8_t*>(ps);
+    tab.g8[q] = static_cast<uint8_t*>(pg);
+    tab.pad[q] = static_cast<uint32_t*>(pp);
+  }
+  CUDA_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(p->win_pad) + kPadTable, &tab, sizeof tab,
+                      cudaMemcpyHostToDevice));
+  // (every peer zeroed its pad before contributing its handles to the all-gather above,
+  // so no signal can land in an uninitialised pad)
+  p->dev.send = p->win_send;
+  p->p2p_ready = true;
+  return FP8LM_OK;
+#else
+  (void)comm; (void)stream;
+  return fail(FP8LM_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+uint8_t* fp8lm_peer_g8(const fp8lm_plan* p) { return (p && p->p2p_ready) ? p->win_g8 : nullptr; }
 
 int64_t fp8lm_plan_offset(const fp8lm_plan* p, int32_t t) {
   if (!p || t < 0 || t >= p->T) return -1;
@@ -309,10 +381,22 @@ static int check_plan(const fp8lm_plan* p, const fp8lm_comm* comm, const char* w
     if (comm->nranks != p->nranks || comm->rank != p->rank)
       return fail(FP8LM_EINVAL, "%s: communicator (%d/%d) does not match plan (%d/%d)", who,
                   comm->rank, comm->nranks, p->rank, p->nranks);
+  } else if (p->mode == FP8LM_MODE_P2P) {
+    if (!p->p2p_ready) return fail(FP8LM_EINVAL, "%s: mode P2P needs fp8lm_peer_setup first", who);
   } else if (comm) {
     return fail(FP8LM_EINVAL, "%s: communicator given but plan mode is not NCCL", who);
   }
   return FP8LM_OK;
+}
+
+static P2PArgs p2p_args(const fp8lm_plan* p, uint32_t epoch) {
+  P2PArgs x;
+  x.tab = reinterpret_cast<const PeerTable*>(reinterpret_cast<uint8_t*>(p->win_pad) + kPadTable);
+  x.pad = p->win_pad;
+  x.rank = p->rank;
+  x.nranks = p->nranks;
+  x.epoch = epoch;
+  return x;
 }
 
 // resolve the gradient source(s): SIMULATED -> host array of nranks device pointers
@@ -377,8 +461,14 @@ int fp8lm_amax_scale_sync(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, in
     return FP8LM_OK;
   }
   const bool nccl = p->mode == FP8LM_MODE_NCCL;
+  if (p->mode == FP8LM_MODE_P2P) {
+    // A1 amax; its last CTA exchanges the local scales through the peers' pads (Eq. 4)
+    const P2PArgs x = p2p_args(p, ++p->epoch);
+    CUDA_TRY(launch_amax(p->dev, srcs, nsrc, src_dtype, mu, amax_out, s_g, skip, true, &x, s));
+    return FP8LM_OK;
+  }
   // A1 amax; its last CTA computes the scales (A2) and, without an exchange, s_g + skip
-  CUDA_TRY(launch_amax(p->dev, srcs, nsrc, src_dtype, mu, amax_out, s_g, skip, !nccl, s));
+  CUDA_TRY(launch_amax(p->dev, srcs, nsrc, src_dtype, mu, amax_out, s_g, skip, !nccl, nullptr, s));
   if (nccl) {
 #ifdef FP8LM_WITH_NCCL
     // Eq. 4: s'_g = min(s'_1, ..., s'_N) — T floats over NVLink
@@ -416,6 +506,12 @@ int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int
     // saturation and its last CTA runs the Eq. 6 / mu tail
     uint8_t* dst[1] = {g8};
     CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, &tail, s));
+  } else if (p->mode == FP8LM_MODE_P2P) {
+    if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "grad_allreduce: mode P2P needs g8 == fp8lm_peer_g8(plan)");
+    uint8_t* dst[1] = {p->win_send};
+    CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, nullptr, s));
+    // A4 + A5 in one kernel over NVLink peer memory (same epoch as this step's amax)
+    CUDA_TRY(launch_reduce_p2p(d, p2p_args(p, p->epoch), g8, s_g, tail, s));
   } else if (p->mode == FP8LM_MODE_SIMULATED) {
     uint8_t* dst[FP8LM_MAX_SIM_RANKS];
     for (int r = 0; r < nsrc; ++r) dst[r] = d.sim_codes + (int64_t)r * p->total;

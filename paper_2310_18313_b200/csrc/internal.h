@@ -42,6 +42,27 @@ struct DevPlan {
 
 constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2;
 
+// ---------------------------------------------------------------- mode P2P windows
+// Signal / exchange pad of one rank (bytes): three flag arrays (one u32 epoch slot per
+// source rank), the peer pointer table, then the exchanged per-tensor data:
+// scales[N][T] (float, local scales for the MIN of Eq. 4) and sat[N][T] (u32,
+// per-shard saturation counts).
+constexpr int kMaxPeers = FP8LM_MAX_P2P_RANKS;
+constexpr size_t kPadFlagScale = 0, kPadFlagReady = 64, kPadFlagDone = 128, kPadTable = 256,
+                 kPadData = 1024;
+struct PeerTable {
+  uint8_t* send[kMaxPeers];
+  uint8_t* g8[kMaxPeers];
+  uint32_t* pad[kMaxPeers];
+};
+struct P2PArgs {
+  const PeerTable* tab;   // device copy inside this rank's pad
+  uint32_t* pad;          // this rank's pad
+  int rank;
+  int nranks;
+  uint32_t epoch;         // step counter: flags hold the epoch of their last signal
+};
+
 // outputs of the Eq. 6 / mu tail of fp8lm_grad_allreduce
 struct TailArgs {
   int nranks;
@@ -72,6 +93,14 @@ struct fp8lm_plan {
   void* ws = nullptr;
   fp8lm::DevPlan dev{};
   bool bound = false;
+  // mode P2P: symmetric windows owned by the plan, peer mappings, step epoch
+  uint8_t* win_send = nullptr;
+  uint8_t* win_g8 = nullptr;
+  uint32_t* win_pad = nullptr;
+  size_t pad_bytes = 0;
+  std::vector<void*> mapped;
+  uint32_t epoch = 0;
+  bool p2p_ready = false;
 };
 
 namespace fp8lm {
@@ -82,7 +111,7 @@ namespace fp8lm {
 enum ProfId : int {
   P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
   P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
-  P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_COUNT
+  P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_COUNT
 };
 bool prof_on();
 struct ProfScope {
@@ -96,7 +125,9 @@ struct ProfScope {
 // kernel launchers (kernels.cu); return cudaError_t of the launch
 cudaError_t launch_amax(const DevPlan& p, const void* const* srcs, int nsrc, int src_dtype,
                         const float* mu, float* amax_out, float* s_out, int32_t* skip,
-                        bool finalize, cudaStream_t s);
+                        bool finalize, const P2PArgs* x, cudaStream_t s);
+cudaError_t launch_reduce_p2p(const DevPlan& p, const P2PArgs& x, uint8_t* g8, const float* s_g,
+                              const TailArgs& tail, cudaStream_t s);
 cudaError_t launch_scale_fix(const DevPlan& p, float* s_g, int32_t* skip, cudaStream_t s);
 cudaError_t launch_quantize(const DevPlan& p, const void* const* srcs, uint8_t* const* dsts,
                             int nsrc, int src_dtype, const float* s_g, const TailArgs* tail,

@@ -33,6 +33,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--lr", type=float, default=3e-4)
+    ap.add_argument("--mode", choices=["nccl", "p2p"], default="nccl")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -41,7 +42,8 @@ def main():
     import paper_2310_18313_b200 as B
 
     comm = B.Comm.from_torch_distributed()
-    plan = B.Plan(NUMELS, mode=B.MODE_NCCL, nranks=N, rank=rank)
+    mode = B.MODE_P2P if args.mode == "p2p" else B.MODE_NCCL
+    plan = B.Plan(NUMELS, mode=mode, nranks=N, rank=rank)
     w0 = plan.flat(torch.float32)
     for t, v in enumerate(plan.views(w0)):
         synth.fill_weights(v, t)
@@ -101,7 +103,7 @@ def main():
     for m in msgs[:10]:
         print(m, flush=True)
     if rank == 0:
-        print(f"NCCL parity N={N}: {'OK' if flag.item() == 1 else 'MISMATCH'}", flush=True)
+        print(f"{args.mode.upper()} parity N={N}: {'OK' if flag.item() == 1 else 'MISMATCH'}", flush=True)
     comm.close()
     dist.destroy_process_group()
     sys.exit(0 if flag.item() == 1 else 1)

@@ -1,7 +1,10 @@
-"""Multi-GPU parity of the NCCL mode (one process per GPU, torchrun), bit-exact against
-the N-rank oracle: amax -> MIN all-reduce of the scales -> E4M3 quantize -> all-to-all
--> rank-order FP32 reduce of the own shard -> in-place all-gather + summed saturation
-counts -> mu -> FP8 AdamW.  Needs >= 2 GPUs (gpurun --gpus 2 / 4)."""
+"""Multi-GPU parity (one process per GPU, torchrun), bit-exact against the N-rank
+oracle, for both exchange modes:
+  nccl: amax -> MIN all-reduce -> quantize -> ncclAlltoAll -> rank-order reduce of the
+        own shard -> in-place ncclAllGather + summed saturation counts -> mu -> AdamW;
+  p2p:  the same arithmetic with the MIN exchanged through peer pads and reduce-scatter
+        + reduce + all-gather fused in one kernel over NVLink peer memory.
+Needs >= 2 GPUs (gpurun --gpus 2 / 4)."""
 import os
 import socket
 import subprocess
@@ -34,13 +37,14 @@ def _port():
     return p
 
 
+@pytest.mark.parametrize("mode", ["nccl", "p2p"])
 @pytest.mark.parametrize("n", [2, 4])
-def test_nccl_mode_bit_exact(n):
+def test_multi_gpu_bit_exact(n, mode):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "dist_worker.py"), "--steps", "3"]
+           os.path.join(ROOT, "tests", "dist_worker.py"), "--steps", "3", "--mode", mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert f"NCCL parity N={n}: OK" in r.stdout
+    assert f"{mode.upper()} parity N={n}: OK" in r.stdout
