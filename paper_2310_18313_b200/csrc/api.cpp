@@ -184,8 +184,8 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
   const bool dist = mode == FP8LM_MODE_NCCL || mode == FP8LM_MODE_P2P;
   if (dist && (rank < 0 || rank >= nranks))
     return fail(FP8LM_EINVAL, "plan_create: rank %d out of range", rank);
-  if (mode == FP8LM_MODE_P2P && nranks > FP8LM_MAX_P2P_RANKS)
-    return fail(FP8LM_EINVAL, "plan_create: mode P2P supports at most %d ranks", FP8LM_MAX_P2P_RANKS);
+  if (mode == FP8LM_MODE_P2P && (nranks < 2 || nranks > FP8LM_MAX_P2P_RANKS))
+    return fail(FP8LM_EINVAL, "plan_create: mode P2P needs 2..%d ranks", FP8LM_MAX_P2P_RANKS);
   for (int t = 0; t < T; ++t)
     if (numels[t] < 0) return fail(FP8LM_EINVAL, "plan_create: numel[%d] < 0", t);
 
