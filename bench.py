@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 METRIC = "FP8 grad reduce+Adam step: GB/s & % HBM/NVLink roofline at 1/2/4/8 B200"
 UNIT = "GB/s"
 FALLBACK_HBM_GBS = 6650.0
+NVLINK_PEER_GBS = 770.0   # measured peer copy per direction per GPU (B200_PROFILING.md)
 
 
 def parse():
@@ -328,7 +329,19 @@ def main():
     ours = {k: v for k, v in prof.items() if v["ours"]}
     dom = max(ours, key=lambda k: ours[k]["ms"]) if ours else None
     roof = None
-    if dom:
+    if dom == "reduce_p2p":
+        # fused reduce-scatter + all-gather over NVLink peer memory: every direction of
+        # every link carries 2(N-1)/N bytes per parameter (read responses + peer stores)
+        per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
+        nvb = 2.0 * (N - 1) / N * params
+        achieved = nvb / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "nvlink", "kernel": dom, "achieved": achieved, "peak": NVLINK_PEER_GBS,
+                "unit": "GB/s", "frac": achieved / NVLINK_PEER_GBS,
+                "peak_kind": "measured peer copy per direction (B200_PROFILING.md); 900 nominal",
+                "frac_of_nominal_900": achieved / 900.0, "traffic": None,
+                "alg_bytes_per_launch": nvb, "avg_launch_ms": per_launch_ms,
+                "share_of_step": ours[dom]["ms"] / (ms_local * args.steps)}
+    elif dom:
         per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
         bpp = KERNEL_BYTES.get(dom)
         if bpp is not None:
