@@ -1,0 +1,121 @@
+#!/usr/bin/env python
+"""Config C5 (BASELINE.json configs[4]): FP8 gradient all-reduce message-size sweep vs
+NCCL bf16, under torchrun on N GPUs of one box.
+
+For every FP8 payload size n (bytes = elements) it times, max over ranks, CUDA events:
+  p2p_full  — amax_scale_sync + fp8_grad_allreduce in mode P2P from an fp32 gradient
+              (amax, MIN of scales through peer pads, quantize, fused peer-memory
+              reduce-scatter + rank-order reduce + all-gather)
+  p2p_xchg  — the fused exchange kernel alone (k_reduce_p2p, library launch tracing)
+  nccl_full — the same arithmetic with NCCL transport (mode NCCL)
+  nccl_bf16 — torch.distributed.all_reduce of n bf16 elements (NCCL, default algorithm)
+  nccl_f32  — the same in fp32
+and prints one JSON line per (size, impl) with time, algbw (payload bytes / time: n for
+FP8, 2n for bf16, 4n for fp32) and busbw = algbw * 2(N-1)/N.
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+        bench_c5.py --min-log2 10 --max-log2 30 --stride 2
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def timed(fn, iters, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item() * 1e3          # us
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--min-log2", type=int, default=10)
+    ap.add_argument("--max-log2", type=int, default=30)
+    ap.add_argument("--stride", type=int, default=2)
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, N = dist.get_rank(), dist.get_world_size()
+    import paper_2310_18313_b200 as B
+    import synth
+
+    comm = B.Comm.from_torch_distributed()
+    busf = 2.0 * (N - 1) / N
+    rows = []
+    for lg in range(args.min_log2, args.max_log2 + 1, args.stride):
+        n = 1 << lg
+        iters = max(5, min(args.iters, int(2e9 // n)))
+        g = torch.empty(n, dtype=torch.float32, device="cuda")
+        synth.fill_gradient(g, 1, 0, rank, amp=1e-3)
+        res = {}
+        for mode_name, mode in (("p2p", B.MODE_P2P), ("nccl", B.MODE_NCCL)):
+            plan = B.Plan([n], mode=mode, nranks=N, rank=rank)
+            if mode == B.MODE_P2P:
+                plan.peer_setup(comm)
+                g8 = plan.peer_g8()
+                c = None
+            else:
+                g8 = plan.flat(torch.uint8, nbytes_like_g8=True)
+                c = comm
+            mu = torch.ones(1, device="cuda")
+            amax = torch.zeros(1, device="cuda")
+            s_g = torch.zeros(1, device="cuda")
+            skip = torch.zeros(1, dtype=torch.int32, device="cuda")
+            gs = torch.zeros(1, device="cuda")
+            gsi = torch.zeros(1, device="cuda")
+            sat = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+            def full():
+                B.amax_scale_sync(plan, g, mu, amax, s_g, skip, comm=c)
+                B.fp8_grad_allreduce(plan, g, s_g, skip, g8, gs, gsi, sat, mu, comm=c)
+
+            B.prof_enable(True)
+            res[f"{mode_name}_full"] = timed(full, iters)
+            B.prof_enable(False)
+            prof = B.prof_read()
+            if mode == B.MODE_P2P and "reduce_p2p" in prof:
+                t = torch.tensor([prof["reduce_p2p"]["ms"] / prof["reduce_p2p"]["launches"]],
+                                 dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                res["p2p_xchg"] = t.item() * 1e3
+            del plan, g8
+        for dt, name, esz in ((torch.bfloat16, "nccl_bf16", 2), (torch.float32, "nccl_f32", 4)):
+            x = torch.ones(n, dtype=dt, device="cuda")
+            res[name] = timed(lambda: dist.all_reduce(x), iters)
+            del x
+        for impl, us in res.items():
+            payload = n * (2 if impl == "nccl_bf16" else 4 if impl == "nccl_f32" else 1)
+            algbw = payload / (us * 1e-6) / 1e9
+            row = {"config": "C5", "n_gpus": N, "elements": n, "fp8_bytes": n, "impl": impl,
+                   "us": us, "algbw_GBs": algbw, "busbw_GBs": algbw * busf,
+                   "busbw_frac_of_900": algbw * busf / 900.0}
+            rows.append(row)
+            if rank == 0:
+                print(json.dumps(row), flush=True)
+        del g
+        torch.cuda.empty_cache()
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
