@@ -224,6 +224,18 @@ int fp8lm_adam_step(fp8lm_plan* plan, const uint8_t* g8, const float* g_scale_in
                     const fp8lm_stensors* master, const fp8lm_stensors* w8,
                     const fp8lm_adam_hp* hp, const int32_t* skip, void* stream);
 
+/* ------------------------------------------------ the whole data-parallel step */
+/* (2) + (3) + (4) in one call, with the fusions the separate calls cannot express;
+ * results are bit-identical to calling fp8lm_amax_scale_sync, fp8lm_grad_allreduce and
+ * fp8lm_adam_step in sequence (same arguments).  Mode LOCAL: the codes of A3 are final
+ * (N = 1), so the quantize kernel also runs Adam pass 1 on them (4 launches per step,
+ * 26 B/param instead of 27).  Other modes: the three calls in sequence. */
+int fp8lm_dp_step(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
+                  float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                  float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
+                  const fp8lm_stensors* v, const fp8lm_stensors* master,
+                  const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, void* stream);
+
 /* Initial optimizer state: m1, v = zero codes with scale 1,
  * amax 0; master / w8 JIT-encoded from the FP32 flat weights w0 (plan layout). */
 int fp8lm_state_init(fp8lm_plan* plan, const float* w0, const fp8lm_stensors* m1,

@@ -80,6 +80,9 @@ _sig("fp8lm_prof_ids", C.c_int)
 _sig("fp8lm_prof_read", C.c_int, _i32, C.POINTER(C.c_char_p), C.POINTER(_i64), C.POINTER(C.c_double),
      C.POINTER(_i32))
 _sig("fp8lm_selftest_fastmath", C.c_int, _u64, _u64, C.POINTER(_u64))
+_sig("fp8lm_dp_step", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
+     C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors),
+     C.POINTER(AdamHP), _p)
 _sig("fp8lm_state_init", C.c_int, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(STensors), C.POINTER(STensors), _p)
 
@@ -364,7 +367,9 @@ class FP8DataParallel:
     scale feed the next forward pass; .mu is already updated for the next step."""
 
     def __init__(self, plan: Plan, w0_flat: torch.Tensor, comm: Comm = None, lr: float = 3e-4,
-                 betas=(0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.1):
+                 betas=(0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.1,
+                 fused: bool = True):
+        self.fused = fused
         self.plan, self.comm = plan, comm
         dev = plan.device
         T = max(plan.T, 1)
@@ -390,6 +395,17 @@ class FP8DataParallel:
     def step(self, grads, lr: float = None, stream=None):
         self.t += 1
         hp = adam_hp(self.lr if lr is None else lr, self.t, self.betas[0], self.betas[1], self.eps, self.wd)
+        if self.fused:
+            g, dt, keep = _grads_arg(self.plan, grads)
+            st = self.state
+            m1, v, w, w8 = st.m1.c(), st.v.c(), st.master.c(), st.w8.c()
+            _check(lib.fp8lm_dp_step(self.plan.handle, self.comm.handle if self.comm else None, g, dt,
+                                     _ptr(self.mu), _ptr(self.amax), _ptr(self.s_g), _ptr(self.skip),
+                                     _ptr(self.g8), _ptr(self.g_scale), _ptr(self.g_scale_inv),
+                                     _ptr(self.sat), C.byref(m1), C.byref(v), C.byref(w),
+                                     C.byref(w8), C.byref(hp), _stream(stream)), "fp8lm_dp_step")
+            del keep
+            return
         amax_scale_sync(self.plan, grads, self.mu, self.amax, self.s_g, self.skip, self.comm, stream)
         fp8_grad_allreduce(self.plan, grads, self.s_g, self.skip, self.g8, self.g_scale,
                            self.g_scale_inv, self.sat, self.mu, self.comm, stream)

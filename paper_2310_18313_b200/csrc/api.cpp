@@ -573,6 +573,33 @@ int fp8lm_adam_step(fp8lm_plan* p, const uint8_t* g8, const float* g_scale_inv,
   return FP8LM_OK;
 }
 
+// ---------------------------------------------------------------- the whole step
+int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
+                  float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                  float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
+                  const fp8lm_stensors* v, const fp8lm_stensors* master,
+                  const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, void* stream) {
+  int rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream);
+  if (rc) return rc;
+  if (p->mode != FP8LM_MODE_LOCAL || p->T == 0) {
+    rc = fp8lm_grad_allreduce(p, comm, grads, src_dtype, s_g, skip, g8, g_scale, g_scale_inv, sat,
+                              mu, stream);
+    if (rc) return rc;
+    return fp8lm_adam_step(p, g8, g_scale_inv, m1, v, master, w8, hp, skip, stream);
+  }
+  // LOCAL: the codes quantize produces are final, so Adam pass 1 runs in the same kernel
+  if ((rc = check_stensors(p, m1, "m1", "dp_step")) || (rc = check_stensors(p, v, "v", "dp_step")) ||
+      (rc = check_stensors(p, master, "master", "dp_step")) ||
+      (rc = check_stensors(p, w8, "w8", "dp_step")))
+    return rc;
+  if (!hp || !g_scale || !g_scale_inv || !sat) return fail(FP8LM_EINVAL, "dp_step: NULL argument");
+  if (!g8 || !aligned(g8, 256)) return fail(FP8LM_EINVAL, "dp_step: g8 NULL or misaligned");
+  const TailArgs tail{1, skip, sat, g_scale, g_scale_inv, mu};
+  CUDA_TRY(launch_adam_fused_local(p->dev, grads, src_dtype, s_g, g8, tail, *m1, *v, *master, *w8,
+                                   *hp, skip, S(stream)));
+  return FP8LM_OK;
+}
+
 int fp8lm_state_init(fp8lm_plan* p, const float* w0, const fp8lm_stensors* m1,
                      const fp8lm_stensors* v, const fp8lm_stensors* master,
                      const fp8lm_stensors* w8, void* stream) {

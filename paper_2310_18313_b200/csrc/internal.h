@@ -111,7 +111,7 @@ namespace fp8lm {
 enum ProfId : int {
   P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
   P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
-  P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_COUNT
+  P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_COUNT
 };
 bool prof_on();
 struct ProfScope {
@@ -141,6 +141,11 @@ cudaError_t launch_adam(const DevPlan& p, const uint8_t* g8, const float* g_sinv
                         const fp8lm_stensors& m1, const fp8lm_stensors& v,
                         const fp8lm_stensors& w, const fp8lm_stensors& w8,
                         const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s);
+cudaError_t launch_adam_fused_local(const DevPlan& p, const void* grads, int src_dtype,
+                                   const float* s_g, uint8_t* g8, const TailArgs& tail,
+                                   const fp8lm_stensors& m1, const fp8lm_stensors& v,
+                                   const fp8lm_stensors& w, const fp8lm_stensors& w8,
+                                   const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s);
 cudaError_t launch_state_init(const DevPlan& p, const float* w0, const fp8lm_stensors& m1,
                               const fp8lm_stensors& v, const fp8lm_stensors& w,
                               const fp8lm_stensors& w8, cudaStream_t s);

@@ -89,7 +89,7 @@ RAGGED = [3, 16, 17, 64, 1000, 16384, 16385, 40000, 70001]
 
 
 def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float32,
-                     specials=None, amp=None, check_tensors=None):
+                     specials=None, amp=None, check_tensors=None, fused=True):
     """Run the device path for `steps` steps and the oracle on the same inputs; compare
     every per-tensor output of every step.  check_tensors: oracle runs only on this
     subset (valid because nothing couples two tensors except the skip flag, and the
@@ -100,7 +100,7 @@ def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float3
     for t, v in enumerate(plan.views(w0)):
         if v.numel():
             synth.fill_weights(v, t)
-    dp = B.FP8DataParallel(plan, w0, lr=lr)
+    dp = B.FP8DataParallel(plan, w0, lr=lr, fused=fused)
     sub = list(range(plan.T)) if check_tensors is None else list(check_tensors)
     ref_all = R.oracle_init(plan, w0)
     ref_states = [ref_all[t] for t in sub]
@@ -145,13 +145,24 @@ def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float3
     return plan, dp
 
 
-def test_local_ragged_multistep(B):
-    """N = 1 (LOCAL): 9 ragged tensors spanning tiles + tails, 6 steps with mu dynamics."""
-    _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=6)
+@pytest.mark.parametrize("fused", [True, False], ids=["dp_step", "three_calls"])
+def test_local_ragged_multistep(B, fused):
+    """N = 1 (LOCAL): 9 ragged tensors spanning tiles + tails, 6 steps with mu dynamics,
+    through fp8lm_dp_step (quantize + Adam pass 1 fused) and through the three calls."""
+    _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=6, fused=fused)
 
 
-def test_local_bf16_gradients(B):
-    _run_and_compare(B, RAGGED[:6], B.MODE_LOCAL, 1, steps=2, dtype=torch.bfloat16)
+@pytest.mark.parametrize("fused", [True, False], ids=["dp_step", "three_calls"])
+def test_local_bf16_gradients(B, fused):
+    _run_and_compare(B, RAGGED[:6], B.MODE_LOCAL, 1, steps=2, dtype=torch.bfloat16, fused=fused)
+
+
+def test_local_fused_skip_and_screen_fallback(B):
+    """Fused LOCAL step: an inf gradient (skip) and a large lr (screen fallback)."""
+    def specials(flat, r, step):
+        if step == 2:
+            flat[11] = float("inf")
+    _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=3, specials=specials, lr=0.05)
 
 
 @pytest.mark.parametrize("N", [2, 3, 8])
