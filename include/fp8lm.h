@@ -68,9 +68,12 @@ typedef enum {
   FP8LM_MODE_SIMULATED = 1,  /* nranks simulated ranks whose gradients all live on this
                                 device (config C1); the exchange is a local read       */
   FP8LM_MODE_NCCL = 2,       /* one process per GPU; exchange over NCCL (NVLink)       */
-  FP8LM_MODE_P2P = 3         /* one process per GPU; the exchange runs inside this
+  FP8LM_MODE_P2P = 3,        /* one process per GPU; the exchange runs inside this
                                 library's kernels over NVLink peer memory (CUDA IPC
                                 windows of fp8lm_peer_setup); NCCL only bootstraps      */
+  FP8LM_MODE_ZERO = 4        /* P2P transport with FP8 ZeRO whole-tensor ownership (Alg. 1,
+                                P:206-237): tensor t is reduced and optimised only by its
+                                owner, which then writes w8 + scale into every rank    */
 } fp8lm_mode;
 
 #define FP8LM_MAX_P2P_RANKS 8     /* ranks of one NVLink / NVSwitch domain in mode P2P */
@@ -146,6 +149,16 @@ size_t fp8lm_plan_workspace_bytes(const fp8lm_plan* plan);
  * EWORKSPACE if ws is NULL / too small / misaligned. */
 int fp8lm_plan_bind(fp8lm_plan* plan, void* ws, size_t ws_bytes, void* stream);
 
+/* Mode ZERO: owner of tensor t (Alg. 1 with the R21 ties), its element offset in this
+ * rank's COMPACT layout of owned tensors (-1 if another rank owns it), and the elements
+ * of that compact layout (the size of the owned g8 / m1 / v / master / w8 buffers).
+ * In mode ZERO the per-tensor state arrays (scale, scale_inv, amax) are indexed by the
+ * owned-tensor ordinal j = 0..fp8lm_plan_owned_count-1 (owned tensors in ascending t). */
+int32_t fp8lm_plan_owner(const fp8lm_plan* plan, int32_t t);
+int64_t fp8lm_plan_owned_offset(const fp8lm_plan* plan, int32_t t);
+int64_t fp8lm_plan_owned_total(const fp8lm_plan* plan);
+int32_t fp8lm_plan_owned_count(const fp8lm_plan* plan);
+
 /* Mode P2P, collective (every rank, after fp8lm_plan_bind): allocate this rank's
  * symmetric windows — the quantized send buffer (N*S bytes), the reduced-code buffer
  * g8 (N*S bytes) and a small signal / exchange pad — exchange their CUDA IPC handles over
@@ -157,6 +170,11 @@ int fp8lm_peer_setup(fp8lm_plan* plan, fp8lm_comm* comm, void* stream);
 /* Mode P2P: this rank's g8 window (device); pass it as g8 to the calls below.  NULL if
  * fp8lm_peer_setup has not run. */
 uint8_t* fp8lm_peer_g8(const fp8lm_plan* plan);
+/* Mode ZERO (also set up by fp8lm_peer_setup): the replicated FP8 weight copy of ALL
+ * tensors in the full layout (every owner writes its tensors' w8 codes here on every
+ * rank) and its per-tensor scalars, three device float[T] rows: scale, scale_inv, amax. */
+uint8_t* fp8lm_peer_w8(const fp8lm_plan* plan);
+float* fp8lm_peer_w8_scalars(const fp8lm_plan* plan);
 
 /* ------------------------------------------- (1) fp8_quantize: one scaling tensor */
 /* App. B JIT scaling + App. A encode.  src: n elements of src_dtype (F32 or BF16),
@@ -200,7 +218,11 @@ int fp8lm_amax_scale_sync(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
  * grads as in (2).  g8: fp8lm_plan_g8_bytes bytes.  All outputs are device arrays [T].
  * Mode P2P: g8 must be fp8lm_peer_g8(plan); one kernel reads every rank's quantized
  * shard over NVLink, reduces in rank order and stores the result into every rank's g8
- * (reduce-scatter + all-gather fused), with sys-scope flag barriers in the peers' pads. */
+ * (reduce-scatter + all-gather fused), with sys-scope flag barriers in the peers' pads.
+ * Mode ZERO: g8 is this rank's COMPACT buffer (fp8lm_plan_owned_total bytes); the kernel
+ * reduces, for each owned tensor, every rank's codes straight from their send windows
+ * (no all-gather: only the owner needs them).  sat / mu / g_scale / g_scale_inv stay
+ * full [T] arrays, replicated on every rank. */
 int fp8lm_grad_allreduce(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
                          int32_t src_dtype, const float* s_g, const int32_t* skip,
                          uint8_t* g8, float* g_scale, float* g_scale_inv, uint32_t* sat,
@@ -218,7 +240,11 @@ int fp8lm_grad_allreduce(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
  *   master <- F16(fl(w' * 65504/A_w)),  w8 <- E4M3(fl(w' * 448/A_w))
  *   (scale = 1 where the amax is 0); each stensor's scale/scale_inv/amax updated.
  * If *skip != 0 nothing changes.  hp is a HOST pointer.  m1/w8 data: uint8 flat,
- * v/master data: uint16 (FP16 bits) flat, all at the plan's offsets. */
+ * v/master data: uint16 (FP16 bits) flat, all at the plan's offsets.
+ * Mode ZERO: g8 and the four states are COMPACT (owned tensors only, scalars indexed
+ * by the owned ordinal; g_scale_inv is the full [T] array); after the update every
+ * owner stores its tensors' w8 codes and scalars into every rank's fp8lm_peer_w8 /
+ * fp8lm_peer_w8_scalars (collective: returns once all ranks' copies have landed). */
 int fp8lm_adam_step(fp8lm_plan* plan, const uint8_t* g8, const float* g_scale_inv,
                     const fp8lm_stensors* m1, const fp8lm_stensors* v,
                     const fp8lm_stensors* master, const fp8lm_stensors* w8,
@@ -237,7 +263,9 @@ int fp8lm_dp_step(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t
                   const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, void* stream);
 
 /* Initial optimizer state: m1, v = zero codes with scale 1,
- * amax 0; master / w8 JIT-encoded from the FP32 flat weights w0 (plan layout). */
+ * amax 0; master / w8 JIT-encoded from the FP32 flat weights w0 (plan layout).
+ * Mode ZERO: w0 and the states are COMPACT (owned tensors); the replicated w8 copy is
+ * then broadcast as after a step (collective). */
 int fp8lm_state_init(fp8lm_plan* plan, const float* w0, const fp8lm_stensors* m1,
                      const fp8lm_stensors* v, const fp8lm_stensors* master,
                      const fp8lm_stensors* w8, void* stream);

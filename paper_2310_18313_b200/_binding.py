@@ -26,7 +26,7 @@ lib = C.CDLL(LIB_PATH)
 # ------------------------------------------------------------------ constants (fp8lm.h)
 OK, EINVAL, ECUDA, ENCCL, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 E4M3, E5M2, F16, BF16, F32 = 0, 1, 2, 3, 4
-MODE_LOCAL, MODE_SIMULATED, MODE_NCCL, MODE_P2P = 0, 1, 2, 3
+MODE_LOCAL, MODE_SIMULATED, MODE_NCCL, MODE_P2P, MODE_ZERO = 0, 1, 2, 3, 4
 ALIGN_ELEMS = 64
 MAX_SIM_RANKS = 16
 
@@ -69,6 +69,12 @@ _sig("fp8lm_plan_workspace_bytes", C.c_size_t, _p)
 _sig("fp8lm_plan_bind", C.c_int, _p, _p, C.c_size_t, _p)
 _sig("fp8lm_peer_setup", C.c_int, _p, _p, _p)
 _sig("fp8lm_peer_g8", _p, _p)
+_sig("fp8lm_peer_w8", _p, _p)
+_sig("fp8lm_peer_w8_scalars", _p, _p)
+_sig("fp8lm_plan_owner", _i32, _p, _i32)
+_sig("fp8lm_plan_owned_offset", _i64, _p, _i32)
+_sig("fp8lm_plan_owned_total", _i64, _p)
+_sig("fp8lm_plan_owned_count", _i32, _p)
 _sig("fp8lm_quantize", C.c_int, _p, _i32, _i64, _i32, _p, _p, _p, _p, _i32, _p, _p)
 _sig("fp8lm_dequantize", C.c_int, _p, _i32, _i64, _p, _p, _p)
 _sig("fp8lm_amax_scale_sync", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p)
@@ -230,16 +236,42 @@ class Plan:
         """Mode P2P: map every rank's windows (collective; see fp8lm_peer_setup)."""
         _check(lib.fp8lm_peer_setup(self.handle, comm.handle, _stream(stream)), "fp8lm_peer_setup")
 
-    def peer_g8(self) -> torch.Tensor:
-        """Mode P2P: this rank's g8 window as a uint8 tensor (no copy)."""
-        ptr = lib.fp8lm_peer_g8(self.handle)
+    def _window(self, ptr, n, typestr):
         if not ptr:
-            raise FP8LMError("peer_g8: fp8lm_peer_setup has not run")
+            raise FP8LMError("peer window missing: fp8lm_peer_setup has not run")
 
         class _Win:
-            __cuda_array_interface__ = {"shape": (self.g8_bytes,), "typestr": "|u1",
-                                        "data": (ptr, False), "version": 3}
+            __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                        "version": 3}
         return torch.as_tensor(_Win(), device=self.device)
+
+    def peer_g8(self) -> torch.Tensor:
+        """Mode P2P: this rank's g8 window as a uint8 tensor (no copy)."""
+        return self._window(lib.fp8lm_peer_g8(self.handle), self.g8_bytes, "|u1")
+
+    def peer_w8(self) -> torch.Tensor:
+        """Mode ZERO: the replicated FP8 weight copy (full layout) as a uint8 tensor."""
+        return self._window(lib.fp8lm_peer_w8(self.handle), max(self.total, 1), "|u1")
+
+    def peer_w8_scalars(self) -> torch.Tensor:
+        """Mode ZERO: [3, T] float rows (scale, scale_inv, amax) of the replicated w8."""
+        return self._window(lib.fp8lm_peer_w8_scalars(self.handle), 3 * self.T, "<f4").view(3, self.T)
+
+    # ---- mode ZERO: the compact layout of the owned tensors
+    def owner(self, t: int) -> int:
+        return lib.fp8lm_plan_owner(self.handle, t)
+
+    def owned(self):
+        """-> list of (t, compact offset) of the tensors this rank owns (ascending t)."""
+        out = []
+        for t in range(self.T):
+            o = lib.fp8lm_plan_owned_offset(self.handle, t)
+            if o >= 0:
+                out.append((t, o))
+        return out
+
+    def compact(self) -> "CompactLayout":
+        return CompactLayout(self)
 
     def shard_begin(self, rank: int) -> int:
         return lib.fp8lm_plan_shard_begin(self.handle, rank)
@@ -258,6 +290,29 @@ class Plan:
 
     def gather(self, flat: torch.Tensor, t: int) -> torch.Tensor:
         return flat[self.offsets[t]: self.offsets[t] + self.numels[t]]
+
+
+class CompactLayout:
+    """Mode ZERO: flat layout of the owned tensors (optimizer state lives only here)."""
+
+    def __init__(self, plan: Plan):
+        self.plan = plan
+        self.device = plan.device
+        self.total = lib.fp8lm_plan_owned_total(plan.handle)
+        self.T = lib.fp8lm_plan_owned_count(plan.handle)
+        self.entries = plan.owned()                    # [(t, offset)]
+        self.numels = [plan.numels[t] for t, _ in self.entries]
+        self.offsets = [o for _, o in self.entries]
+
+    def flat(self, dtype) -> torch.Tensor:
+        return torch.zeros(max(self.total, 1), dtype=dtype, device=self.device)
+
+    def gather(self, full_flat: torch.Tensor) -> torch.Tensor:
+        """compact copy of the owned tensors of a full-layout buffer"""
+        out = self.flat(full_flat.dtype)
+        for (t, o), n in zip(self.entries, self.numels):
+            out[o:o + n] = self.plan.gather(full_flat, t)
+        return out
 
 
 class STensorSet:
@@ -378,16 +433,25 @@ class FP8DataParallel:
         self.amax = torch.zeros(nsim * T, dtype=torch.float32, device=dev)
         self.s_g = torch.zeros(T, dtype=torch.float32, device=dev)
         self.skip = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.layout = plan
         if plan.mode == MODE_P2P:
             plan.peer_setup(comm)
             self.g8 = plan.peer_g8()
             self.comm = None            # the exchange runs in the library's kernels
+        elif plan.mode == MODE_ZERO:
+            plan.peer_setup(comm)
+            self.comm = None
+            self.layout = plan.compact()               # optimizer state: owned tensors only
+            self.g8 = self.layout.flat(torch.uint8)
+            w0_flat = self.layout.gather(w0_flat)
+            self.w8_full = plan.peer_w8()
+            self.w8_full_scalars = plan.peer_w8_scalars()
         else:
             self.g8 = plan.flat(torch.uint8, nbytes_like_g8=True)
         self.g_scale = torch.zeros(T, dtype=torch.float32, device=dev)
         self.g_scale_inv = torch.zeros(T, dtype=torch.float32, device=dev)
         self.sat = torch.zeros(T, dtype=torch.int32, device=dev)
-        self.state = OptimizerState(plan)
+        self.state = OptimizerState(self.layout)
         state_init(plan, w0_flat, self.state)
         self.lr, self.betas, self.eps, self.wd = lr, betas, eps, weight_decay
         self.t = 0

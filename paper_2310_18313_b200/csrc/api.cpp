@@ -174,18 +174,19 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
                       int32_t rank, fp8lm_plan** out) {
   if (!out) return fail(FP8LM_EINVAL, "plan_create: out is NULL");
   if (T < 0 || (T > 0 && !numels)) return fail(FP8LM_EINVAL, "plan_create: bad T / numels");
-  if (mode < FP8LM_MODE_LOCAL || mode > FP8LM_MODE_P2P)
+  if (mode < FP8LM_MODE_LOCAL || mode > FP8LM_MODE_ZERO)
     return fail(FP8LM_EINVAL, "plan_create: bad mode %d", mode);
   if (nranks < 1) return fail(FP8LM_EINVAL, "plan_create: nranks must be >= 1");
   if (mode == FP8LM_MODE_LOCAL && nranks != 1)
     return fail(FP8LM_EINVAL, "plan_create: mode LOCAL needs nranks == 1");
   if (mode == FP8LM_MODE_SIMULATED && nranks > FP8LM_MAX_SIM_RANKS)
     return fail(FP8LM_EINVAL, "plan_create: at most %d simulated ranks", FP8LM_MAX_SIM_RANKS);
-  const bool dist = mode == FP8LM_MODE_NCCL || mode == FP8LM_MODE_P2P;
+  const bool peer = mode == FP8LM_MODE_P2P || mode == FP8LM_MODE_ZERO;
+  const bool dist = mode == FP8LM_MODE_NCCL || peer;
   if (dist && (rank < 0 || rank >= nranks))
     return fail(FP8LM_EINVAL, "plan_create: rank %d out of range", rank);
-  if (mode == FP8LM_MODE_P2P && (nranks < 2 || nranks > FP8LM_MAX_P2P_RANKS))
-    return fail(FP8LM_EINVAL, "plan_create: mode P2P needs 2..%d ranks", FP8LM_MAX_P2P_RANKS);
+  if (peer && (nranks < 2 || nranks > FP8LM_MAX_P2P_RANKS))
+    return fail(FP8LM_EINVAL, "plan_create: modes P2P / ZERO need 2..%d ranks", FP8LM_MAX_P2P_RANKS);
   for (int t = 0; t < T; ++t)
     if (numels[t] < 0) return fail(FP8LM_EINVAL, "plan_create: numel[%d] < 0", t);
 
@@ -240,6 +241,30 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
     p->off_recv = take((size_t)(p->shard * nranks));
   }
   if (mode == FP8LM_MODE_SIMULATED) p->off_sim = take((size_t)(p->total * nranks));
+  if (mode == FP8LM_MODE_ZERO) {
+    // Alg. 1: whole tensors to owners; this rank keeps optimizer state only
+    // for its own tensors, packed in a compact LOCAL sub-plan
+    p->owner.resize(std::max(T, 1));
+    std::vector<int64_t> load(nranks);
+    fp8lm_zero_plan(T, numels, nranks, p->owner.data(), load.data());
+    std::vector<int64_t> own_numel;
+    for (int t = 0; t < T; ++t)
+      if (p->owner[t] == p->rank) {
+        p->own2full.push_back(t);
+        p->own_gpos.push_back(p->offset[t]);
+        own_numel.push_back(p->numel[t]);
+      }
+    int rc = fp8lm_plan_create((int32_t)own_numel.size(), own_numel.data(), FP8LM_MODE_LOCAL, 1, 0,
+                               &p->own);
+    if (rc) { delete p; return rc; }
+    p->full2own_off.assign(std::max(T, 1), -1);
+    for (size_t j = 0; j < p->own2full.size(); ++j) p->full2own_off[p->own2full[j]] = p->own->offset[j];
+    const size_t To = std::max<size_t>(p->own2full.size(), 1);
+    p->off_own_ws = take(p->own->ws_bytes);
+    p->off_own_gpos = take(sizeof(int64_t) * To);
+    p->off_own2full = take(sizeof(int32_t) * To);
+    p->off_gsinv_own = take(sizeof(float) * To);
+  }
   p->ws_bytes = off;
   *out = p;
   return FP8LM_OK;
@@ -251,13 +276,31 @@ int fp8lm_plan_destroy(fp8lm_plan* plan) {
   if (plan->win_send) cudaFree(plan->win_send);
   if (plan->win_g8) cudaFree(plan->win_g8);
   if (plan->win_pad) cudaFree(plan->win_pad);
+  if (plan->win_w8) cudaFree(plan->win_w8);
+  if (plan->own) fp8lm_plan_destroy(plan->own);
   delete plan;
   return FP8LM_OK;
 }
 
+int32_t fp8lm_plan_owner(const fp8lm_plan* p, int32_t t) {
+  if (!p || p->mode != FP8LM_MODE_ZERO || t < 0 || t >= p->T) return -1;
+  return p->owner[t];
+}
+int64_t fp8lm_plan_owned_offset(const fp8lm_plan* p, int32_t t) {
+  if (!p || p->mode != FP8LM_MODE_ZERO || t < 0 || t >= p->T) return -1;
+  return p->full2own_off[t];
+}
+int64_t fp8lm_plan_owned_total(const fp8lm_plan* p) {
+  return (p && p->mode == FP8LM_MODE_ZERO) ? p->own->total : -1;
+}
+int32_t fp8lm_plan_owned_count(const fp8lm_plan* p) {
+  return (p && p->mode == FP8LM_MODE_ZERO) ? (int32_t)p->own2full.size() : -1;
+}
+
 // ---------------------------------------------------------------- mode P2P windows
 int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
-  if (!p || p->mode != FP8LM_MODE_P2P) return fail(FP8LM_EINVAL, "peer_setup: plan mode is not P2P");
+  if (!p || (p->mode != FP8LM_MODE_P2P && p->mode != FP8LM_MODE_ZERO))
+    return fail(FP8LM_EINVAL, "peer_setup: plan mode is not P2P / ZERO");
   if (!p->bound) return fail(FP8LM_EWORKSPACE, "peer_setup: plan not bound");
   if (p->p2p_ready) return FP8LM_OK;
 #ifdef FP8LM_WITH_NCCL
@@ -265,17 +308,20 @@ int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
     return fail(FP8LM_EINVAL, "peer_setup: communicator does not match the plan");
   const int N = p->nranks;
   const size_t win = (size_t)p->g8_bytes;
-  p->pad_bytes = kPadData + (size_t)N * std::max(p->T, 1) * (sizeof(float) + sizeof(uint32_t));
+  p->pad_bytes = pad_bytes_for(N, p->T);
+  const bool zero = p->mode == FP8LM_MODE_ZERO;
   CUDA_TRY(cudaMalloc(&p->win_send, win));
-  CUDA_TRY(cudaMalloc(&p->win_g8, win));
+  CUDA_TRY(cudaMalloc(&p->win_g8, zero ? 256 : win));     // ZERO: the owner's g8 is compact
+  CUDA_TRY(cudaMalloc(&p->win_w8, zero ? std::max<size_t>(p->total, 256) : 256));
   CUDA_TRY(cudaMalloc(&p->win_pad, p->pad_bytes));
   CUDA_TRY(cudaMemset(p->win_pad, 0, p->pad_bytes));
   CUDA_TRY(cudaMemset(p->win_send, 0, win));
-  struct Handles { cudaIpcMemHandle_t send, g8, pad; };
+  struct Handles { cudaIpcMemHandle_t send, g8, pad, w8; };
   Handles mine;
   CUDA_TRY(cudaIpcGetMemHandle(&mine.send, p->win_send));
   CUDA_TRY(cudaIpcGetMemHandle(&mine.g8, p->win_g8));
   CUDA_TRY(cudaIpcGetMemHandle(&mine.pad, p->win_pad));
+  CUDA_TRY(cudaIpcGetMemHandle(&mine.w8, p->win_w8));
   Handles* dev = nullptr;
   CUDA_TRY(cudaMalloc(&dev, sizeof(Handles) * N));
   CUDA_TRY(cudaMemcpy(dev + p->rank, &mine, sizeof(Handles), cudaMemcpyHostToDevice));
@@ -291,18 +337,22 @@ int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
       tab.send[q] = p->win_send;
       tab.g8[q] = p->win_g8;
       tab.pad[q] = p->win_pad;
+      tab.w8[q] = p->win_w8;
       continue;
     }
-    void *ps = nullptr, *pg = nullptr, *pp = nullptr;
+    void *ps = nullptr, *pg = nullptr, *pp = nullptr, *pw = nullptr;
     CUDA_TRY(cudaIpcOpenMemHandle(&ps, all[q].send, cudaIpcMemLazyEnablePeerAccess));
     p->mapped.push_back(ps);
     CUDA_TRY(cudaIpcOpenMemHandle(&pg, all[q].g8, cudaIpcMemLazyEnablePeerAccess));
     p->mapped.push_back(pg);
     CUDA_TRY(cudaIpcOpenMemHandle(&pp, all[q].pad, cudaIpcMemLazyEnablePeerAccess));
     p->mapped.push_back(pp);
+    CUDA_TRY(cudaIpcOpenMemHandle(&pw, all[q].w8, cudaIpcMemLazyEnablePeerAccess));
+    p->mapped.push_back(pw);
     tab.send[q] = static_cast<uint8_t*>(ps);
     tab.g8[q] = static_cast<uint8_t*>(pg);
     tab.pad[q] = static_cast<uint32_t*>(pp);
+    tab.w8[q] = static_cast<uint8_t*>(pw);
   }
   CUDA_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(p->win_pad) + kPadTable, &tab, sizeof tab,
                       cudaMemcpyHostToDevice));
@@ -317,7 +367,17 @@ int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
 #endif
 }
 
-uint8_t* fp8lm_peer_g8(const fp8lm_plan* p) { return (p && p->p2p_ready) ? p->win_g8 : nullptr; }
+uint8_t* fp8lm_peer_g8(const fp8lm_plan* p) {
+  return (p && p->p2p_ready && p->mode == FP8LM_MODE_P2P) ? p->win_g8 : nullptr;
+}
+uint8_t* fp8lm_peer_w8(const fp8lm_plan* p) {
+  return (p && p->p2p_ready && p->mode == FP8LM_MODE_ZERO) ? p->win_w8 : nullptr;
+}
+float* fp8lm_peer_w8_scalars(const fp8lm_plan* p) {
+  if (!(p && p->p2p_ready && p->mode == FP8LM_MODE_ZERO)) return nullptr;
+  return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(p->win_pad) + kPadData +
+                                  (size_t)p->nranks * p->T * 8);
+}
 
 int64_t fp8lm_plan_offset(const fp8lm_plan* p, int32_t t) {
   if (!p || t < 0 || t >= p->T) return -1;
@@ -367,6 +427,21 @@ int fp8lm_plan_bind(fp8lm_plan* p, void* ws, size_t ws_bytes, void* stream) {
   d.sim_codes = p->mode == FP8LM_MODE_SIMULATED ? b + p->off_sim : nullptr;
   d.sat_acc = reinterpret_cast<uint32_t*>(b + p->off_sat_acc);
   d.counters = reinterpret_cast<uint32_t*>(b + p->off_ctr);
+  d.T_own = 0;
+  if (p->mode == FP8LM_MODE_ZERO) {
+    int rc = fp8lm_plan_bind(p->own, b + p->off_own_ws, p->own->ws_bytes, stream);
+    if (rc) return rc;
+    const size_t To = p->own2full.size();
+    if (To) {
+      CUDA_TRY(cudaMemcpyAsync(b + p->off_own_gpos, p->own_gpos.data(), sizeof(int64_t) * To, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(b + p->off_own2full, p->own2full.data(), sizeof(int32_t) * To, cudaMemcpyHostToDevice, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    d.T_own = (int32_t)To;
+    d.own_gpos = reinterpret_cast<const int64_t*>(b + p->off_own_gpos);
+    d.own2full = reinterpret_cast<const int32_t*>(b + p->off_own2full);
+    d.gsinv_own = reinterpret_cast<float*>(b + p->off_gsinv_own);
+  }
   p->ws = ws;
   p->bound = true;
   return FP8LM_OK;
@@ -381,8 +456,8 @@ static int check_plan(const fp8lm_plan* p, const fp8lm_comm* comm, const char* w
     if (comm->nranks != p->nranks || comm->rank != p->rank)
       return fail(FP8LM_EINVAL, "%s: communicator (%d/%d) does not match plan (%d/%d)", who,
                   comm->rank, comm->nranks, p->rank, p->nranks);
-  } else if (p->mode == FP8LM_MODE_P2P) {
-    if (!p->p2p_ready) return fail(FP8LM_EINVAL, "%s: mode P2P needs fp8lm_peer_setup first", who);
+  } else if (p->mode == FP8LM_MODE_P2P || p->mode == FP8LM_MODE_ZERO) {
+    if (!p->p2p_ready) return fail(FP8LM_EINVAL, "%s: modes P2P / ZERO need fp8lm_peer_setup first", who);
   } else if (comm) {
     return fail(FP8LM_EINVAL, "%s: communicator given but plan mode is not NCCL", who);
   }
@@ -461,7 +536,7 @@ int fp8lm_amax_scale_sync(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, in
     return FP8LM_OK;
   }
   const bool nccl = p->mode == FP8LM_MODE_NCCL;
-  if (p->mode == FP8LM_MODE_P2P) {
+  if (p->mode == FP8LM_MODE_P2P || p->mode == FP8LM_MODE_ZERO) {
     // A1 amax; its last CTA exchanges the local scales through the peers' pads (Eq. 4)
     const P2PArgs x = p2p_args(p, ++p->epoch);
     CUDA_TRY(launch_amax(p->dev, srcs, nsrc, src_dtype, mu, amax_out, s_g, skip, true, &x, s));
@@ -506,6 +581,11 @@ int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int
     // saturation and its last CTA runs the Eq. 6 / mu tail
     uint8_t* dst[1] = {g8};
     CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, &tail, s));
+  } else if (p->mode == FP8LM_MODE_ZERO) {
+    uint8_t* dst[1] = {p->win_send};
+    CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, nullptr, s));
+    // each owner reduces its whole tensors from every rank's send window
+    CUDA_TRY(launch_reduce_owner(d, p->own->dev, p2p_args(p, p->epoch), g8, s_g, tail, s));
   } else if (p->mode == FP8LM_MODE_P2P) {
     if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "grad_allreduce: mode P2P needs g8 == fp8lm_peer_g8(plan)");
     uint8_t* dst[1] = {p->win_send};
@@ -568,6 +648,16 @@ int fp8lm_adam_step(fp8lm_plan* p, const uint8_t* g8, const float* g_scale_inv,
       (rc = check_stensors(p, master, "master", "adam_step")) || (rc = check_stensors(p, w8, "w8", "adam_step")))
     return rc;
   if (!hp || !skip || !g_scale_inv) return fail(FP8LM_EINVAL, "adam_step: NULL hp / skip / g_scale_inv");
+  if (p->mode == FP8LM_MODE_ZERO) {
+    // ZeRO: AdamW on the owned tensors (compact sub-plan), then the owners write w8 into
+    // every rank's replicated copy
+    if (!p->p2p_ready) return fail(FP8LM_EINVAL, "adam_step: mode ZERO needs fp8lm_peer_setup first");
+    if (p->own->T > 0 && (!g8 || !aligned(g8, 256))) return fail(FP8LM_EINVAL, "adam_step: g8 NULL or misaligned");
+    CUDA_TRY(launch_adam(p->own->dev, g8, p->dev.gsinv_own, *m1, *v, *master, *w8, *hp, skip, S(stream)));
+    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p, ++p->epoch_w8),
+                             static_cast<const uint8_t*>(w8->data), *w8, S(stream)));
+    return FP8LM_OK;
+  }
   if (p->T > 0 && (!g8 || !aligned(g8, 256))) return fail(FP8LM_EINVAL, "adam_step: g8 NULL or misaligned");
   CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream)));
   return FP8LM_OK;
@@ -609,6 +699,14 @@ int fp8lm_state_init(fp8lm_plan* p, const float* w0, const fp8lm_stensors* m1,
   if ((rc = check_stensors(p, m1, "m1", "state_init")) || (rc = check_stensors(p, v, "v", "state_init")) ||
       (rc = check_stensors(p, master, "master", "state_init")) || (rc = check_stensors(p, w8, "w8", "state_init")))
     return rc;
+  if (p->mode == FP8LM_MODE_ZERO) {
+    if (!p->p2p_ready) return fail(FP8LM_EINVAL, "state_init: mode ZERO needs fp8lm_peer_setup first");
+    if (p->own->T > 0 && (!w0 || !aligned(w0, 256))) return fail(FP8LM_EINVAL, "state_init: w0 NULL or misaligned");
+    CUDA_TRY(launch_state_init(p->own->dev, w0, *m1, *v, *master, *w8, S(stream)));
+    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p, ++p->epoch_w8),
+                             static_cast<const uint8_t*>(w8->data), *w8, S(stream)));
+    return FP8LM_OK;
+  }
   if (p->T > 0 && (!w0 || !aligned(w0, 256))) return fail(FP8LM_EINVAL, "state_init: w0 NULL or misaligned");
   CUDA_TRY(launch_state_init(p->dev, w0, *m1, *v, *master, *w8, S(stream)));
   return FP8LM_OK;

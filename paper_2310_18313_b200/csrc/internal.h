@@ -38,6 +38,11 @@ struct DevPlan {
   uint8_t* sim_codes;       // [nsim*total] simulated ranks' quantized codes
   uint32_t* sat_acc;        // [T]       saturation counts of the step (zero at rest)
   uint32_t* counters;       // [4]       grid_last_block tickets (zero at rest)
+  // mode ZERO: owned tensors j = 0..T_own-1 (ascending t)
+  int32_t T_own;
+  const int64_t* own_gpos;  // [T_own] full-layout offset of owned tensor j
+  const int32_t* own2full;  // [T_own] its global index t
+  float* gsinv_own;         // [T_own] compact copy of g_scale_inv (written by the reduce tail)
 };
 
 constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2;
@@ -48,13 +53,18 @@ constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2;
 // scales[N][T] (float, local scales for the MIN of Eq. 4) and sat[N][T] (u32,
 // per-shard saturation counts).
 constexpr int kMaxPeers = FP8LM_MAX_P2P_RANKS;
-constexpr size_t kPadFlagScale = 0, kPadFlagReady = 64, kPadFlagDone = 128, kPadTable = 256,
-                 kPadData = 1024;
+constexpr size_t kPadFlagScale = 0, kPadFlagReady = 64, kPadFlagDone = 128, kPadFlagW8 = 192,
+                 kPadTable = 256, kPadData = 1024;
 struct PeerTable {
   uint8_t* send[kMaxPeers];
   uint8_t* g8[kMaxPeers];
   uint32_t* pad[kMaxPeers];
+  uint8_t* w8[kMaxPeers];   // mode ZERO: replicated FP8 weight copy (full layout)
 };
+// pad data region: scales [N][T] f32 | sat [N][T] u32 | (ZERO) w8 scalars [3][T] f32
+inline size_t pad_bytes_for(int N, int T) {
+  return kPadData + (size_t)N * (T > 0 ? T : 1) * 8 + (size_t)3 * (T > 0 ? T : 1) * 4;
+}
 struct P2PArgs {
   const PeerTable* tab;   // device copy inside this rank's pad
   uint32_t* pad;          // this rank's pad
@@ -100,7 +110,14 @@ struct fp8lm_plan {
   size_t pad_bytes = 0;
   std::vector<void*> mapped;
   uint32_t epoch = 0;
+  uint32_t epoch_w8 = 0;
   bool p2p_ready = false;
+  uint8_t* win_w8 = nullptr;
+  // mode ZERO: Alg. 1 owners, the owned tensors and the compact sub-plan over them
+  std::vector<int32_t> owner, own2full;
+  std::vector<int64_t> own_gpos, full2own_off;
+  fp8lm_plan* own = nullptr;
+  size_t off_own_ws = 0, off_own_gpos = 0, off_own2full = 0, off_gsinv_own = 0;
 };
 
 namespace fp8lm {
@@ -111,7 +128,7 @@ namespace fp8lm {
 enum ProfId : int {
   P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
   P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
-  P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_COUNT
+  P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_W8_BCAST, P_COUNT
 };
 bool prof_on();
 struct ProfScope {
@@ -128,6 +145,12 @@ cudaError_t launch_amax(const DevPlan& p, const void* const* srcs, int nsrc, int
                         bool finalize, const P2PArgs* x, cudaStream_t s);
 cudaError_t launch_reduce_p2p(const DevPlan& p, const P2PArgs& x, uint8_t* g8, const float* s_g,
                               const TailArgs& tail, cudaStream_t s);
+// mode ZERO: owner reduce over the compact sub-plan `o` (items), tails on the full plan `p`
+cudaError_t launch_reduce_owner(const DevPlan& p, const DevPlan& o, const P2PArgs& x, uint8_t* g8,
+                                const float* s_g, const TailArgs& tail, cudaStream_t s);
+// mode ZERO: owned w8 codes (compact) + scalars -> every rank's w8 window / pad rows
+cudaError_t launch_w8_bcast(const DevPlan& p, const DevPlan& o, const P2PArgs& x,
+                            const uint8_t* w8_own, const fp8lm_stensors& w8s, cudaStream_t s);
 cudaError_t launch_scale_fix(const DevPlan& p, float* s_g, int32_t* skip, cudaStream_t s);
 cudaError_t launch_quantize(const DevPlan& p, const void* const* srcs, uint8_t* const* dsts,
                             int nsrc, int src_dtype, const float* s_g, const TailArgs* tail,

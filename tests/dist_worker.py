@@ -29,11 +29,34 @@ F32 = np.float32
 NUMELS = [3, 16, 17, 64, 1000, 16384, 16385, 40000, 70001, 5]
 
 
+def check_zero(B, plan, dp, t, ref, where):
+    """Mode ZERO: the owner's compact states of t, and every rank's replicated w8 of t."""
+    w8 = dp.w8_full.cpu().numpy()[plan.offsets[t]: plan.offsets[t] + plan.numels[t]]
+    sc = dp.w8_full_scalars.cpu().numpy()
+    assert np.array_equal(w8, ref.w8.codes), f"{where}: replicated w8 differs"
+    assert (F32(sc[0, t]), F32(sc[1, t]), F32(sc[2, t])) == (ref.w8.scale, ref.w8.scale_inv, ref.w8.amax), \
+        f"{where}: replicated w8 scalars differ"
+    if plan.owner(t) != dist.get_rank():
+        return
+    j = [tt for tt, _ in dp.layout.entries].index(t)
+    o, n = dp.layout.offsets[j], plan.numels[t]
+    st = dp.state
+    got = dict(
+        m1=st.m1.data[o:o + n].cpu().numpy(),
+        v=st.v.data[o:o + n].cpu().view(torch.int16).numpy().view(np.uint16),
+        master=st.master.data[o:o + n].cpu().view(torch.int16).numpy().view(np.uint16),
+        w8=st.w8.data[o:o + n].cpu().numpy())
+    for k in ("m1", "v", "master", "w8"):
+        s_ = getattr(st, k)
+        got[k + "_s"] = (F32(s_.scale[j].item()), F32(s_.scale_inv[j].item()), F32(s_.amax[j].item()))
+    R.assert_state_equal(got, ref, where)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--lr", type=float, default=3e-4)
-    ap.add_argument("--mode", choices=["nccl", "p2p"], default="nccl")
+    ap.add_argument("--mode", choices=["nccl", "p2p", "zero"], default="nccl")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -42,7 +65,7 @@ def main():
     import paper_2310_18313_b200 as B
 
     comm = B.Comm.from_torch_distributed()
-    mode = B.MODE_P2P if args.mode == "p2p" else B.MODE_NCCL
+    mode = {"p2p": B.MODE_P2P, "nccl": B.MODE_NCCL, "zero": B.MODE_ZERO}[args.mode]
     plan = B.Plan(NUMELS, mode=mode, nranks=N, rank=rank)
     w0 = plan.flat(torch.float32)
     for t, v in enumerate(plan.views(w0)):
@@ -68,7 +91,7 @@ def main():
         per_rank = [[g[plan.offsets[t]: plan.offsets[t] + plan.numels[t]] for t in range(plan.T)]
                     for g in gnp]
         res = OS.train_step(per_rank, mus, ref_states, OA.hyper_params(args.lr, step))
-        g8 = dp.g8.cpu().numpy()
+        g8 = dp.g8.cpu().numpy() if args.mode != "zero" else None
         s_g = dp.s_g.cpu().numpy()
         sat = dp.sat.cpu().numpy()
         mu = dp.mu.cpu().numpy()
@@ -79,8 +102,16 @@ def main():
         for t in range(plan.T):
             p = res["per_tensor"][t]
             sl = slice(plan.offsets[t], plan.offsets[t] + plan.numels[t])
+            if g8 is not None:
+                codes_ok = np.array_equal(g8[sl], p["codes"])
+            elif plan.owner(t) == rank:                       # ZeRO: only the owner reduces t
+                j = [tt for tt, _ in dp.layout.entries].index(t)
+                o = dp.layout.offsets[j]
+                codes_ok = np.array_equal(dp.g8.cpu().numpy()[o:o + plan.numels[t]], p["codes"])
+            else:
+                codes_ok = True
             checks = [
-                ("codes", np.array_equal(g8[sl], p["codes"])),
+                ("codes", codes_ok),
                 ("s_g", F32(s_g[t]) == p["s_g"]),
                 ("sat", int(sat[t]) == p["sat"]),
                 ("scale", F32(gs[t]) == p["scale"]),
@@ -91,8 +122,11 @@ def main():
                     ok = False
                     msgs.append(f"rank {rank} step {step} tensor {t}: {name} differs")
             try:
-                R.assert_state_equal(R.state_np(B, plan, dp.state, t), res["states"][t],
-                                     f"rank {rank} step {step} tensor {t}")
+                if args.mode == "zero":
+                    check_zero(B, plan, dp, t, res["states"][t], f"rank {rank} step {step} tensor {t}")
+                else:
+                    R.assert_state_equal(R.state_np(B, plan, dp.state, t), res["states"][t],
+                                         f"rank {rank} step {step} tensor {t}")
             except AssertionError as e:
                 ok = False
                 msgs.append(str(e)[:300])

@@ -3,7 +3,9 @@ oracle, for both exchange modes:
   nccl: amax -> MIN all-reduce -> quantize -> ncclAlltoAll -> rank-order reduce of the
         own shard -> in-place ncclAllGather + summed saturation counts -> mu -> AdamW;
   p2p:  the same arithmetic with the MIN exchanged through peer pads and reduce-scatter
-        + reduce + all-gather fused in one kernel over NVLink peer memory.
+        + reduce + all-gather fused in one kernel over NVLink peer memory;
+  zero: FP8 ZeRO (Alg. 1): the owner of each whole tensor reduces it from every rank's
+        send window and runs AdamW on it alone; w8 + scalars replicated by peer stores.
 Needs >= 2 GPUs (gpurun --gpus 2 / 4)."""
 import os
 import socket
@@ -37,7 +39,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("mode", ["nccl", "p2p"])
+@pytest.mark.parametrize("mode", ["nccl", "p2p", "zero"])
 @pytest.mark.parametrize("n", [2, 4])
 def test_multi_gpu_bit_exact(n, mode):
     if _ngpus() < n:
