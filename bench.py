@@ -46,9 +46,10 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="gpt-125m", choices=["gpt-125m", "gpt-7b", "gpt-13b"])
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"], help="gradient dtype")
-    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
-                    help="N > 1: fused peer-memory reduce-scatter/all-gather kernel (p2p) or "
-                         "NCCL all-to-all + all-gather around the reduce kernel (nccl)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl", "zero"],
+                    help="N > 1: fused peer-memory reduce-scatter/all-gather kernel (p2p), "
+                         "NCCL all-to-all + all-gather around the reduce kernel (nccl), or "
+                         "FP8 ZeRO whole-tensor owners over peer memory (zero, config C4)")
     ap.add_argument("--lr", type=float, default=6e-4)   # GPT-125M max LR, Table 1
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -60,9 +61,14 @@ def parse():
     return ap.parse_args()
 
 
-def alg_bytes_per_param(N: int) -> float:
+def alg_bytes_per_param(N: int, zero: bool = False) -> float:
     """A1 4 + A3 5 + A7 18 at N = 1 (A4/A5 identity); at N >= 2 add the
-    reduce (1 + 1/N) and the all-gather write 2(N-1)/N."""
+    reduce (1 + 1/N) and the all-gather write 2(N-1)/N.  ZeRO owner mode (C4): every rank
+    reads its gradient twice (A1 4, A3 5), the owner reduce reads N x n/N codes and writes
+    n/N (1 + 1/N), AdamW runs on n/N parameters (18/N) and the w8 broadcast reads n/N and
+    writes n (1/N + 1): 11 + 20/N."""
+    if zero:
+        return 11.0 + 20.0 / N
     if N == 1:
         return 27.0
     return 28.0 + 1.0 / N + 2.0 * (N - 1) / N
@@ -71,6 +77,7 @@ def alg_bytes_per_param(N: int) -> float:
 # per-launch algorithmic bytes per parameter of each kernel (LOCAL / NCCL modes)
 KERNEL_BYTES = {
     "amax": 4.0, "quantize": 5.0, "adam_pass1": 6.0, "adam_pass2": 12.0,
+    "quantize+adam_pass1": 10.0,      # fused LOCAL kernel: read g 4, m1 1, v 2, master 2; write g8 1
 }
 
 
@@ -173,8 +180,12 @@ def max_over_ranks(x: float, world: int) -> float:
 def oracle_sample(specs, config):
     """Bounded sample of the workload for the CPU oracle: the tensors of the first
     layer(s) (~10-20 s of single-core oracle work for GPT-125M)."""
-    want = ("layer0.", "layer1.") if config == "gpt-125m" else ("layer0.ln", "layer0.qkv", "layer0.proj")
-    return [t for t, s in enumerate(specs) if s.name.startswith(want)]
+    if config == "gpt-125m":
+        want = ("layer0.", "layer1.")
+        return [t for t, s in enumerate(specs) if s.name.startswith(want)]
+    # larger models: layer 0's LayerNorms and biases plus its attention projection
+    return [t for t, s in enumerate(specs)
+            if s.name.startswith("layer0.") and (len(s.shape) == 1 or s.name == "layer0.proj.w")]
 
 
 def run_oracle_step(specs, idx, rank, step, states):
@@ -267,13 +278,15 @@ def main():
     params = sum(numels)
     N = world
     comm = B.Comm.from_torch_distributed() if N > 1 else None
-    mode = (B.MODE_P2P if args.exchange == "p2p" else B.MODE_NCCL) if N > 1 else B.MODE_LOCAL
+    mode = ({"p2p": B.MODE_P2P, "nccl": B.MODE_NCCL, "zero": B.MODE_ZERO}[args.exchange]
+            if N > 1 else B.MODE_LOCAL)
+    zero = mode == B.MODE_ZERO
     plan = B.Plan(numels, mode=mode, nranks=N, rank=rank)
     gdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     w0 = plan.flat(torch.float32)
     for t, v in enumerate(plan.views(w0)):
         synth.fill_weights(v, t)
-    R = args.grad_sets or (4 if args.config == "gpt-125m" else 2)
+    R = args.grad_sets or {"gpt-125m": 4, "gpt-7b": 2, "gpt-13b": 1}[args.config]
     gsets = []
     for r_ in range(R):
         g = plan.flat(gdt)
@@ -319,7 +332,7 @@ def main():
     ms_local = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms_local, world)
 
-    bytes_rank = alg_bytes_per_param(N) * params * (1.0 if args.dtype == "f32" else 1.0)
+    bytes_rank = alg_bytes_per_param(N, zero) * params
     if args.dtype == "bf16":
         bytes_rank -= 2.0 * 2 * params      # A1 and A3 read 2 B instead of 4
     value = N * bytes_rank / (ms / 1e3) / 1e9
@@ -329,11 +342,13 @@ def main():
     ours = {k: v for k, v in prof.items() if v["ours"]}
     dom = max(ours, key=lambda k: ours[k]["ms"]) if ours else None
     roof = None
+    kparams = sum(dp.layout.numels) if zero else params     # AdamW runs on owned tensors only
     if dom == "reduce_p2p":
         # fused reduce-scatter + all-gather over NVLink peer memory: every direction of
-        # every link carries 2(N-1)/N bytes per parameter (read responses + peer stores)
+        # every link carries 2(N-1)/N bytes per parameter (read responses + peer stores);
+        # the ZeRO owner reduce only pulls (N-1)/N (the w8 broadcast is a separate kernel)
         per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
-        nvb = 2.0 * (N - 1) / N * params
+        nvb = (1.0 if zero else 2.0) * (N - 1) / N * params
         achieved = nvb / (per_launch_ms / 1e3) / 1e9
         roof = {"bound": "nvlink", "kernel": dom, "achieved": achieved, "peak": NVLINK_PEER_GBS,
                 "unit": "GB/s", "frac": achieved / NVLINK_PEER_GBS,
@@ -347,10 +362,11 @@ def main():
         if bpp is not None:
             if args.dtype == "bf16" and dom in ("amax", "quantize"):
                 bpp -= 2.0
-            achieved = bpp * params / (per_launch_ms / 1e3) / 1e9
+            np_ = kparams if dom.startswith("adam") else params
+            achieved = bpp * np_ / (per_launch_ms / 1e3) / 1e9
             roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "peak_kind": hbm_kind, "traffic": None,
-                    "alg_bytes_per_launch": bpp * params, "avg_launch_ms": per_launch_ms,
+                    "alg_bytes_per_launch": bpp * np_, "avg_launch_ms": per_launch_ms,
                     "share_of_step": ours[dom]["ms"] / (ms_local * args.steps)}
     launches = int(sum(v["launches"] for v in ours.values()) / args.steps)
     breakdown = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
@@ -400,7 +416,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": f"{args.config} full gradient set (BASELINE.json configs["
-                                   f"{ {'gpt-125m': 1, 'gpt-7b': 2, 'gpt-13b': 3}[args.config] }])",
+                                   f"{ {'gpt-125m': 1, 'gpt-7b': 2, 'gpt-13b': 3}[args.config] }])"
+                                   + (", ZeRO owner mode (Alg. 1)" if zero else ""),
                        "tensors": plan.T, "params": params, "grad_dtype": args.dtype,
                        "alg_bytes_per_param_per_rank": bytes_rank / params,
                        "parallelism": f"dp{N}" if N > 1 else "single", "state_scaling": "jit",
