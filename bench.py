@@ -376,7 +376,8 @@ def main():
     e2e = None
     if not args.no_e2e and not args.quick:
         host_sets = []
-        for g in gsets:
+        # large models: one pinned host copy (the H2D cost per step is the same)
+        for g in (gsets if gsets[0].numel() * gsets[0].element_size() < 4e9 else gsets[:1]):
             h = torch.empty(g.numel(), dtype=gdt, pin_memory=True)
             h.copy_(g)
             host_sets.append(h)
@@ -386,7 +387,7 @@ def main():
         ne = [0]
 
         def e2e_step():
-            grads.copy_(host_sets[ne[0] % R], non_blocking=True)
+            grads.copy_(host_sets[ne[0] % len(host_sets)], non_blocking=True)
             ne[0] += 1
             dp.step(grads)
             torch.cat([dp.mu, dp.s_g, dp.sat.float(), dp.skip.float()], out=out_d)
