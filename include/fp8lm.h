@@ -255,7 +255,9 @@ int fp8lm_adam_step(fp8lm_plan* plan, const uint8_t* g8, const float* g_scale_in
  * results are bit-identical to calling fp8lm_amax_scale_sync, fp8lm_grad_allreduce and
  * fp8lm_adam_step in sequence (same arguments).  Mode LOCAL: the codes of A3 are final
  * (N = 1), so the quantize kernel also runs Adam pass 1 on them (4 launches per step,
- * 26 B/param instead of 27).  Other modes: the three calls in sequence. */
+ * 26 B/param instead of 27).  Mode P2P: the exchange kernel runs Adam pass 1 on the
+ * elements of its own shard (1/N of pass 1 per rank) and combines the ranks' partial
+ * state maxima through the pads.  Other modes: the three calls in sequence. */
 int fp8lm_dp_step(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
                   float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
                   float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,

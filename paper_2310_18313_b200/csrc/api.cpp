@@ -671,11 +671,31 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
                   const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, void* stream) {
   int rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream);
   if (rc) return rc;
-  if (p->mode != FP8LM_MODE_LOCAL || p->T == 0) {
+  if ((p->mode != FP8LM_MODE_LOCAL && p->mode != FP8LM_MODE_P2P) || p->T == 0) {
     rc = fp8lm_grad_allreduce(p, comm, grads, src_dtype, s_g, skip, g8, g_scale, g_scale_inv, sat,
                               mu, stream);
     if (rc) return rc;
     return fp8lm_adam_step(p, g8, g_scale_inv, m1, v, master, w8, hp, skip, stream);
+  }
+  if (p->mode == FP8LM_MODE_P2P) {
+    // the exchange kernel runs Adam pass 1 on its own shard; maxima combined in its tail
+    if ((rc = check_stensors(p, m1, "m1", "dp_step")) || (rc = check_stensors(p, v, "v", "dp_step")) ||
+        (rc = check_stensors(p, master, "master", "dp_step")) ||
+        (rc = check_stensors(p, w8, "w8", "dp_step")))
+      return rc;
+    if (!hp || !g_scale || !g_scale_inv || !sat) return fail(FP8LM_EINVAL, "dp_step: NULL argument");
+    if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "dp_step: mode P2P needs g8 == fp8lm_peer_g8(plan)");
+    const void* srcs[1];
+    int nsrc = 0;
+    if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
+    const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
+    uint8_t* dst[1] = {p->win_send};
+    CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
+    CUDA_TRY(launch_reduce_p2p_a1(p->dev, p2p_args(p, p->epoch), s_g, tail, g8, *m1, *v, *master, *w8,
+                                  *hp, skip, S(stream)));
+    CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream),
+                         /*pass1=*/false));
+    return FP8LM_OK;
   }
   // LOCAL: the codes quantize produces are final, so Adam pass 1 runs in the same kernel
   if ((rc = check_stensors(p, m1, "m1", "dp_step")) || (rc = check_stensors(p, v, "v", "dp_step")) ||

@@ -61,9 +61,11 @@ struct PeerTable {
   uint32_t* pad[kMaxPeers];
   uint8_t* w8[kMaxPeers];   // mode ZERO: replicated FP8 weight copy (full layout)
 };
-// pad data region: scales [N][T] f32 | sat [N][T] u32 | (ZERO) w8 scalars [3][T] f32
+// pad data region: scales [N][T] f32 | sat [N][T] u32 | (ZERO) w8 scalars [3][T] f32 |
+// pass-1 state maxima [N][3T] u32 (fused P2P step)
 inline size_t pad_bytes_for(int N, int T) {
-  return kPadData + (size_t)N * (T > 0 ? T : 1) * 8 + (size_t)3 * (T > 0 ? T : 1) * 4;
+  const size_t t = T > 0 ? T : 1;
+  return kPadData + (size_t)N * t * 8 + 3 * t * 4 + (size_t)N * 3 * t * 4;
 }
 struct P2PArgs {
   const PeerTable* tab;   // device copy inside this rank's pad
@@ -163,12 +165,19 @@ cudaError_t launch_allreduce_finalize(const DevPlan& p, const float* s_g, const 
 cudaError_t launch_adam(const DevPlan& p, const uint8_t* g8, const float* g_sinv,
                         const fp8lm_stensors& m1, const fp8lm_stensors& v,
                         const fp8lm_stensors& w, const fp8lm_stensors& w8,
-                        const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s);
+                        const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s,
+                        bool pass1 = true);
 cudaError_t launch_adam_fused_local(const DevPlan& p, const void* grads, int src_dtype,
                                    const float* s_g, uint8_t* g8, const TailArgs& tail,
                                    const fp8lm_stensors& m1, const fp8lm_stensors& v,
                                    const fp8lm_stensors& w, const fp8lm_stensors& w8,
                                    const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s);
+// mode P2P fused step: exchange + reduce + Adam pass 1 on the own shard (+ maxima exchange)
+cudaError_t launch_reduce_p2p_a1(const DevPlan& p, const P2PArgs& x, const float* s_g,
+                                 const TailArgs& tail, uint8_t* g8, const fp8lm_stensors& m1,
+                                 const fp8lm_stensors& v, const fp8lm_stensors& w,
+                                 const fp8lm_stensors& w8, const fp8lm_adam_hp& hp,
+                                 const int32_t* skip, cudaStream_t s);
 cudaError_t launch_state_init(const DevPlan& p, const float* w0, const fp8lm_stensors& m1,
                               const fp8lm_stensors& v, const fp8lm_stensors& w,
                               const fp8lm_stensors& w8, cudaStream_t s);

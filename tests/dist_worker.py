@@ -57,6 +57,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--lr", type=float, default=3e-4)
     ap.add_argument("--mode", choices=["nccl", "p2p", "zero"], default="nccl")
+    ap.add_argument("--unfused", action="store_true",
+                    help="the three ABI calls instead of fp8lm_dp_step")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -70,7 +72,7 @@ def main():
     w0 = plan.flat(torch.float32)
     for t, v in enumerate(plan.views(w0)):
         synth.fill_weights(v, t)
-    dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr)
+    dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr, fused=not args.unfused)
     ref_states = R.oracle_init(plan, w0)
     mus = [F32(1.0)] * plan.T
     ok = True
@@ -137,7 +139,8 @@ def main():
     for m in msgs[:10]:
         print(m, flush=True)
     if rank == 0:
-        print(f"{args.mode.upper()} parity N={N}: {'OK' if flag.item() == 1 else 'MISMATCH'}", flush=True)
+        tag = args.mode.upper() + ("_UNFUSED" if args.unfused else "")
+        print(f"{tag} parity N={N}: {'OK' if flag.item() == 1 else 'MISMATCH'}", flush=True)
     comm.close()
     dist.destroy_process_group()
     sys.exit(0 if flag.item() == 1 else 1)
