@@ -162,3 +162,71 @@ def adam_step(g_hat: np.ndarray, st: OptState, hp: AdamHP, skip: bool = False) -
 def bytes_per_param(master: int = 2, grad: int = 1, m1: int = 1, m2: int = 2) -> int:
     """Eq. 7 / Eq. 8 accounting."""
     return master + grad + m1 + m2
+
+
+# ---------------------------------------------------------------- delayed state scaling
+# App. B (P:795): "selecting the scaling factor based on the maximum absolute values
+# observed in a certain number of preceding iterations ... necessitates the storage of a
+# history of maximum values".  Reading R25-R27 (DESIGN.md §3): the new state scales are
+# fixed BEFORE the update, so AdamW becomes ONE pass (12 B/param instead of 18):
+#   m1 (E4M3): s_m = 448 / B_m, B_m an a-priori bound on |m'| from the current scales
+#              (|m| <= 448 m_sinv, |g| <= 448 g_sinv): never saturates (R25);
+#   v  (FP16): s_v = 65504 / B_v, B_v = beta2 65504 v_sinv + (1-beta2) (448 g_sinv)^2 (R25);
+#   master (FP16): s_w = 65504 / (16 H_w), w8 (E4M3): s_8 = 448 / H_w, where H_w is the
+#              maximum of the last HIST exact amax(w') values (R26; 16x headroom costs the
+#              FP16 master no precision, the w8 copy saturates like any delayed scaling).
+# The exact amax of the new values is still recorded (history, diagnostics) (R27).
+HIST = 16                              # history length (SPEC S:150)
+W_HEADROOM = F32(16.0)
+BOUND_SLACK = F32(1.0 + 2.0 ** -20)    # covers the binary32 roundings of the bound itself
+
+
+def delayed_scales(st: OptState, g_scale_inv: np.float32, hp: AdamHP, w_hist) -> tuple:
+    """(s_m, s_v, s_w, s_8), each a binary32 op sequence (the kernel's, R25-R26)."""
+    gsi = F32(g_scale_inv)
+    b_m = F32(F32(F32(hp.beta1 * E4M3_MAX) * F32(st.m1.scale_inv)) +
+              F32(F32(hp.one_minus_beta1 * E4M3_MAX) * gsi))
+    b_m = F32(b_m * BOUND_SLACK)
+    G = F32(E4M3_MAX * gsi)
+    b_v = F32(F32(F32(hp.beta2 * FP16_MAX) * F32(st.v.scale_inv)) +
+              F32(F32(hp.one_minus_beta2 * G) * G))
+    b_v = F32(b_v * BOUND_SLACK)
+    h_w = F32(np.max(np.asarray(w_hist, dtype=np.float32)))
+    return (jit_scale(b_m, E4M3_MAX), jit_scale(b_v, FP16_MAX),
+            jit_scale(F32(h_w * W_HEADROOM), FP16_MAX), jit_scale(h_w, E4M3_MAX))
+
+
+def encode_with(x: np.ndarray, fmt, s: np.float32, a: np.float32) -> ScaledTensor:
+    codes = encode(np.asarray(x, dtype=np.float32) * F32(s), fmt)   # fl(x * s)
+    return ScaledTensor(codes, fmt, F32(s), F32(F32(1.0) / F32(s)), F32(a))
+
+
+def init_history(st: OptState) -> np.ndarray:
+    """Ring of HIST exact amax(w) values; starts with amax(w0)."""
+    h = np.zeros(HIST, dtype=np.float32)
+    h[0] = st.master.amax
+    return h
+
+
+def adam_step_delayed(g_hat: np.ndarray, st: OptState, hp: AdamHP, g_scale_inv: np.float32,
+                      w_hist: np.ndarray, step: int, skip: bool = False) -> Dict:
+    """One FP8 AdamW step with delayed state scaling (one pass).  ``step`` >= 1 selects the
+    history slot (step - 1) % HIST that receives this step's exact amax(w').
+    Returns dict(state, hist, m, v, w, scales)."""
+    if skip:
+        return dict(state=st.copy(), hist=np.array(w_hist, np.float32), m=None, v=None, w=None)
+    s_m, s_v, s_w, s_8 = delayed_scales(st, g_scale_inv, hp, w_hist)
+    g = np.asarray(g_hat, dtype=np.float32)
+    m_new, v_new, w_new = adam_math(g, st.m1.value(), st.v.value(), st.master.value(), hp)
+    am = F32(np.abs(m_new).max()) if m_new.size else F32(0.0)
+    av = F32(v_new.max()) if v_new.size else F32(0.0)
+    aw = F32(np.abs(w_new).max()) if w_new.size else F32(0.0)
+    new = OptState(
+        m1=encode_with(m_new, E4M3, s_m, am),
+        v=encode_with(v_new, FP16, s_v, av),
+        master=encode_with(w_new, FP16, s_w, aw),
+        w8=encode_with(w_new, E4M3, s_8, aw),
+    )
+    hist = np.array(w_hist, dtype=np.float32)
+    hist[(step - 1) % HIST] = aw
+    return dict(state=new, hist=hist, m=m_new, v=v_new, w=w_new, scales=(s_m, s_v, s_w, s_8))

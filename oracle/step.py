@@ -22,8 +22,11 @@ from . import pipeline as P
 
 
 def train_step(grads_by_rank: List[List[np.ndarray]], mus: List[np.float32],
-               states: List[A.OptState], hp: A.AdamHP, run_adam: bool = True):
-    """grads_by_rank[r][t] -> dict(per_tensor=[...], skip, mu_next=[...], states=[...])."""
+               states: List[A.OptState], hp: A.AdamHP, run_adam: bool = True,
+               hists=None, step: int = 1):
+    """grads_by_rank[r][t] -> dict(per_tensor=[...], skip, mu_next=[...], states=[...]).
+    hists (list of amax(w) rings): delayed state scaling (App. B, P:795) instead of JIT;
+    the updated rings are returned as "hists"."""
     N = len(grads_by_rank)
     T = len(grads_by_rank[0])
     per = []
@@ -34,10 +37,15 @@ def train_step(grads_by_rank: List[List[np.ndarray]], mus: List[np.float32],
     for t in range(T):
         p = per[t]
         p["g_hat"] = P.dequantize(p["codes"], p["scale_inv"])
-        if run_adam:
+        if run_adam and hists is not None:
+            res = A.adam_step_delayed(p["g_hat"], states[t], hp, p["scale_inv"], hists[t], step, skip)
+            p["adam"] = res
+            new_states.append(res["state"])
+        elif run_adam:
             res = A.adam_step(p["g_hat"], states[t], hp, skip)
             p["adam"] = res
             new_states.append(res["state"])
     mu_next = [P.mu_update(mus[t], per[t]["sat"], per[t]["n"], skip) for t in range(T)]
     return dict(per_tensor=per, skip=skip, mu_next=mu_next,
-                states=new_states if run_adam else states)
+                states=new_states if run_adam else states,
+                hists=[p["adam"]["hist"] for p in per] if (run_adam and hists is not None) else None)

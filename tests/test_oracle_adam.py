@@ -5,6 +5,7 @@ import numpy as np
 import torch
 
 from oracle import adam as A
+from oracle import adam as OA
 from oracle.codec import E4M3, FP16, decode
 
 F32 = np.float32
@@ -114,3 +115,67 @@ def test_skip_leaves_state():
     res = A.adam_step(np.full(64, np.nan, np.float32), st, A.hyper_params(1e-3, 1), skip=True)
     assert np.array_equal(res["state"].master.codes, st.master.codes)
     assert res["state"].master.scale == st.master.scale
+
+
+# ---------------------------------------------------------------- delayed state scaling
+def _random_state(rng, n, step_scale=1.0):
+    w0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    st = OA.init_state(w0)
+    hist = OA.init_history(st)
+    for t in range(1, 4):                        # a few JIT steps: non-trivial m1 / v
+        g = (rng.standard_t(3, size=n) * 1e-3 * step_scale).astype(np.float32)
+        st = OA.adam_step(g, st, OA.hyper_params(1e-3, t))["state"]
+    return st, hist
+
+
+def test_delayed_bounds_never_saturate_moments():
+    """R25: the a-priori bounds put |m'| and v' at or below the format max — no code of m1
+    or v ever saturates, on random states and on the equality case (aligned extremes)."""
+    rng = np.random.default_rng(31)
+    for trial in range(30):
+        n = 5000
+        st, hist = _random_state(rng, n, 10.0 ** rng.uniform(-2, 2))
+        gsi = np.float32(10.0 ** rng.uniform(-9, -5))
+        codes = rng.integers(-448, 449, size=n).astype(np.float32)
+        if trial % 3 == 0:                       # extremes of m and g aligned
+            codes[0] = 448.0
+            st.m1.codes[0] = 0x7E
+        g = (decode(OA.encode(codes, E4M3), E4M3).astype(np.float32) * gsi).astype(np.float32)
+        res = OA.adam_step_delayed(g, st, OA.hyper_params(1e-3, 5), gsi, hist, 5)
+        s_m, s_v, _, _ = res["scales"]
+        assert np.all(np.abs(res["m"].astype(np.float64) * s_m) <= 448.0 * (1 + 2 ** -22))
+        assert np.all(res["v"].astype(np.float64) * s_v <= 65504.0 * (1 + 2 ** -22))
+
+
+def test_delayed_encoding_half_ulp_and_history_ring():
+    rng = np.random.default_rng(32)
+    st, hist = _random_state(rng, 20000)
+    g = (rng.standard_t(3, size=20000) * 1e-3).astype(np.float32)
+    gsi = np.float32(np.abs(g).max() / 448.0)
+    hist = hist.copy()
+    for step in range(1, 20):
+        res = OA.adam_step_delayed(g, st, OA.hyper_params(1e-3, step), gsi, hist, step)
+        new = res["state"]
+        for stt, x, fmt in ((new.m1, res["m"], E4M3), (new.v, res["v"], FP16), (new.master, res["w"], FP16)):
+            scaled = x.astype(np.float64) * float(stt.scale)
+            dec = decode(stt.codes, fmt)
+            assert np.all(np.abs(dec - scaled) <= _half_ulp(scaled, fmt) + 1e-7 * np.abs(scaled))
+        # exact amax recorded; slot (step-1) % 16 of the ring receives it
+        assert new.master.amax == np.float32(np.abs(res["w"]).max())
+        assert res["hist"][(step - 1) % OA.HIST] == new.master.amax
+        others = [i for i in range(OA.HIST) if i != (step - 1) % OA.HIST]
+        assert np.array_equal(res["hist"][others], hist[others])
+        # master keeps 16x headroom over the history maximum: never saturates here
+        assert np.max(np.abs(decode(new.master.codes, FP16))) < 65504.0 / 8
+        st, hist = new, res["hist"]
+
+
+def test_delayed_update_arithmetic_is_the_jit_one():
+    """Delayed scaling changes only the encoding: m', v', w' equal the JIT step's."""
+    rng = np.random.default_rng(33)
+    st, hist = _random_state(rng, 3000)
+    g = (rng.standard_normal(3000) * 1e-3).astype(np.float32)
+    a = OA.adam_step(g, st, OA.hyper_params(1e-3, 4))
+    b = OA.adam_step_delayed(g, st, OA.hyper_params(1e-3, 4), np.float32(1e-6), hist, 4)
+    for k in ("m", "v", "w"):
+        assert np.array_equal(a[k], b[k])
