@@ -250,6 +250,20 @@ int fp8lm_adam_step(fp8lm_plan* plan, const uint8_t* g8, const float* g_scale_in
                     const fp8lm_stensors* master, const fp8lm_stensors* w8,
                     const fp8lm_adam_hp* hp, const int32_t* skip, void* stream);
 
+/* Delayed state scaling (App. B: "maximum absolute values observed in a certain
+ * number of preceding iterations"; readings R25-R27): ONE AdamW pass, 12 B/param
+ * instead of 18.  The new scales are fixed before the update: m1 and v from a-priori
+ * bounds on |m'| and v' (they never saturate), master (16x headroom) and w8 from the
+ * maximum of w_hist; the exact new amaxes are still recorded and amax(w') is written
+ * into slot hist_slot of w_hist.  w_hist: device float[16 * T] (ring of exact amax(w')
+ * values, slot-major; start it with amax(w0) in slot 0 and zeros elsewhere);
+ * hist_slot = (step - 1) % 16.  Mode ZERO: w_hist and states are compact (owned). */
+int fp8lm_adam_step_delayed(fp8lm_plan* plan, const uint8_t* g8, const float* g_scale_inv,
+                            const fp8lm_stensors* m1, const fp8lm_stensors* v,
+                            const fp8lm_stensors* master, const fp8lm_stensors* w8,
+                            const fp8lm_adam_hp* hp, const int32_t* skip, float* w_hist,
+                            int32_t hist_slot, void* stream);
+
 /* ------------------------------------------------ the whole data-parallel step */
 /* (2) + (3) + (4) in one call, with the fusions the separate calls cannot express;
  * results are bit-identical to calling fp8lm_amax_scale_sync, fp8lm_grad_allreduce and
@@ -257,12 +271,15 @@ int fp8lm_adam_step(fp8lm_plan* plan, const uint8_t* g8, const float* g_scale_in
  * (N = 1), so the quantize kernel also runs Adam pass 1 on them (4 launches per step,
  * 26 B/param instead of 27).  Mode P2P: the exchange kernel runs Adam pass 1 on the
  * elements of its own shard (1/N of pass 1 per rank) and combines the ranks' partial
- * state maxima through the pads.  Other modes: the three calls in sequence. */
+ * state maxima through the pads.  Other modes: the three calls in sequence.
+ * w_hist != NULL selects delayed state scaling (fp8lm_adam_step_delayed semantics); in
+ * mode LOCAL the quantize kernel then also runs the single AdamW pass (20 B/param). */
 int fp8lm_dp_step(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
                   float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
                   float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
                   const fp8lm_stensors* v, const fp8lm_stensors* master,
-                  const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, void* stream);
+                  const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
+                  int32_t hist_slot, void* stream);
 
 /* Initial optimizer state: m1, v = zero codes with scale 1,
  * amax 0; master / w8 JIT-encoded from the FP32 flat weights w0 (plan layout).

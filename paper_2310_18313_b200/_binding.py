@@ -88,7 +88,9 @@ _sig("fp8lm_prof_read", C.c_int, _i32, C.POINTER(C.c_char_p), C.POINTER(_i64), C
 _sig("fp8lm_selftest_fastmath", C.c_int, _u64, _u64, C.POINTER(_u64))
 _sig("fp8lm_dp_step", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
      C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors),
-     C.POINTER(AdamHP), _p)
+     C.POINTER(AdamHP), _p, _i32, _p)
+_sig("fp8lm_adam_step_delayed", C.c_int, _p, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
+     C.POINTER(STensors), C.POINTER(STensors), C.POINTER(AdamHP), _p, _p, _i32, _p)
 _sig("fp8lm_state_init", C.c_int, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(STensors), C.POINTER(STensors), _p)
 
@@ -407,6 +409,15 @@ def fp8_adam_step(plan: Plan, g8: torch.Tensor, g_scale_inv: torch.Tensor, st: O
            "fp8lm_adam_step")
 
 
+def fp8_adam_step_delayed(plan: Plan, g8: torch.Tensor, g_scale_inv: torch.Tensor, st: OptimizerState,
+                          hp: AdamHP, skip: torch.Tensor, w_hist: torch.Tensor, hist_slot: int,
+                          stream=None):
+    m1, v, w, w8 = st.m1.c(), st.v.c(), st.master.c(), st.w8.c()
+    _check(lib.fp8lm_adam_step_delayed(plan.handle, _ptr(g8), _ptr(g_scale_inv), C.byref(m1), C.byref(v),
+                                       C.byref(w), C.byref(w8), C.byref(hp), _ptr(skip), _ptr(w_hist),
+                                       hist_slot, _stream(stream)), "fp8lm_adam_step_delayed")
+
+
 def state_init(plan: Plan, w0_flat: torch.Tensor, st: OptimizerState, stream=None):
     m1, v, w, w8 = st.m1.c(), st.v.c(), st.master.c(), st.w8.c()
     _check(lib.fp8lm_state_init(plan.handle, _ptr(w0_flat), C.byref(m1), C.byref(v), C.byref(w),
@@ -423,8 +434,10 @@ class FP8DataParallel:
 
     def __init__(self, plan: Plan, w0_flat: torch.Tensor, comm: Comm = None, lr: float = 3e-4,
                  betas=(0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.1,
-                 fused: bool = True):
+                 fused: bool = True, state_scaling: str = "jit"):
         self.fused = fused
+        assert state_scaling in ("jit", "delayed")
+        self.delayed = state_scaling == "delayed"
         self.plan, self.comm = plan, comm
         dev = plan.device
         T = max(plan.T, 1)
@@ -453,6 +466,11 @@ class FP8DataParallel:
         self.sat = torch.zeros(T, dtype=torch.int32, device=dev)
         self.state = OptimizerState(self.layout)
         state_init(plan, w0_flat, self.state)
+        self.w_hist = None
+        if self.delayed:      # amax(w) history ring [16][T]: amax(w0) in slot 0 (R26)
+            Tl = max(self.layout.T, 1)
+            self.w_hist = torch.zeros(16 * Tl, dtype=torch.float32, device=dev)
+            self.w_hist[:Tl].copy_(self.state.master.amax[:Tl])
         self.lr, self.betas, self.eps, self.wd = lr, betas, eps, weight_decay
         self.t = 0
 
@@ -467,10 +485,15 @@ class FP8DataParallel:
                                      _ptr(self.mu), _ptr(self.amax), _ptr(self.s_g), _ptr(self.skip),
                                      _ptr(self.g8), _ptr(self.g_scale), _ptr(self.g_scale_inv),
                                      _ptr(self.sat), C.byref(m1), C.byref(v), C.byref(w),
-                                     C.byref(w8), C.byref(hp), _stream(stream)), "fp8lm_dp_step")
+                                     C.byref(w8), C.byref(hp), _ptr(self.w_hist), (self.t - 1) % 16,
+                                     _stream(stream)), "fp8lm_dp_step")
             del keep
             return
         amax_scale_sync(self.plan, grads, self.mu, self.amax, self.s_g, self.skip, self.comm, stream)
         fp8_grad_allreduce(self.plan, grads, self.s_g, self.skip, self.g8, self.g_scale,
                            self.g_scale_inv, self.sat, self.mu, self.comm, stream)
-        fp8_adam_step(self.plan, self.g8, self.g_scale_inv, self.state, hp, self.skip, stream)
+        if self.delayed:
+            fp8_adam_step_delayed(self.plan, self.g8, self.g_scale_inv, self.state, hp, self.skip,
+                                  self.w_hist, (self.t - 1) % 16, stream)
+        else:
+            fp8_adam_step(self.plan, self.g8, self.g_scale_inv, self.state, hp, self.skip, stream)

@@ -663,18 +663,55 @@ int fp8lm_adam_step(fp8lm_plan* p, const uint8_t* g8, const float* g_scale_inv,
   return FP8LM_OK;
 }
 
+int fp8lm_adam_step_delayed(fp8lm_plan* p, const uint8_t* g8, const float* g_scale_inv,
+                            const fp8lm_stensors* m1, const fp8lm_stensors* v,
+                            const fp8lm_stensors* master, const fp8lm_stensors* w8,
+                            const fp8lm_adam_hp* hp, const int32_t* skip, float* w_hist,
+                            int32_t hist_slot, void* stream) {
+  if (!p) return fail(FP8LM_EINVAL, "adam_step_delayed: plan is NULL");
+  if (!p->bound) return fail(FP8LM_EWORKSPACE, "adam_step_delayed: plan not bound");
+  int rc;
+  if ((rc = check_stensors(p, m1, "m1", "adam_step_delayed")) ||
+      (rc = check_stensors(p, v, "v", "adam_step_delayed")) ||
+      (rc = check_stensors(p, master, "master", "adam_step_delayed")) ||
+      (rc = check_stensors(p, w8, "w8", "adam_step_delayed")))
+    return rc;
+  if (!hp || !skip || !g_scale_inv || !w_hist)
+    return fail(FP8LM_EINVAL, "adam_step_delayed: NULL hp / skip / g_scale_inv / w_hist");
+  if (hist_slot < 0 || hist_slot >= 16) return fail(FP8LM_EINVAL, "adam_step_delayed: hist_slot not in [0, 16)");
+  if (p->mode == FP8LM_MODE_ZERO) {
+    if (!p->p2p_ready) return fail(FP8LM_EINVAL, "adam_step_delayed: mode ZERO needs fp8lm_peer_setup first");
+    CUDA_TRY(launch_adam_delayed(p->own->dev, g8, p->dev.gsinv_own, *m1, *v, *master, *w8, *hp, skip,
+                                 w_hist, hist_slot, S(stream)));
+    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p, ++p->epoch_w8),
+                             static_cast<const uint8_t*>(w8->data), *w8, S(stream)));
+    return FP8LM_OK;
+  }
+  if (p->T > 0 && (!g8 || !aligned(g8, 256))) return fail(FP8LM_EINVAL, "adam_step_delayed: g8 NULL or misaligned");
+  CUDA_TRY(launch_adam_delayed(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, w_hist,
+                               hist_slot, S(stream)));
+  return FP8LM_OK;
+}
+
 // ---------------------------------------------------------------- the whole step
 int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
                   float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
                   float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
                   const fp8lm_stensors* v, const fp8lm_stensors* master,
-                  const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, void* stream) {
+                  const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
+                  int32_t hist_slot, void* stream) {
   int rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream);
   if (rc) return rc;
-  if ((p->mode != FP8LM_MODE_LOCAL && p->mode != FP8LM_MODE_P2P) || p->T == 0) {
+  const bool delayed = w_hist != nullptr;
+  if (delayed && (hist_slot < 0 || hist_slot >= 16)) return fail(FP8LM_EINVAL, "dp_step: hist_slot not in [0, 16)");
+  if ((p->mode != FP8LM_MODE_LOCAL && p->mode != FP8LM_MODE_P2P) || p->T == 0 ||
+      (delayed && p->mode != FP8LM_MODE_LOCAL)) {
     rc = fp8lm_grad_allreduce(p, comm, grads, src_dtype, s_g, skip, g8, g_scale, g_scale_inv, sat,
                               mu, stream);
     if (rc) return rc;
+    if (delayed)
+      return fp8lm_adam_step_delayed(p, g8, g_scale_inv, m1, v, master, w8, hp, skip, w_hist,
+                                     hist_slot, stream);
     return fp8lm_adam_step(p, g8, g_scale_inv, m1, v, master, w8, hp, skip, stream);
   }
   if (p->mode == FP8LM_MODE_P2P) {
@@ -706,7 +743,7 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
   if (!g8 || !aligned(g8, 256)) return fail(FP8LM_EINVAL, "dp_step: g8 NULL or misaligned");
   const TailArgs tail{1, skip, sat, g_scale, g_scale_inv, mu};
   CUDA_TRY(launch_adam_fused_local(p->dev, grads, src_dtype, s_g, g8, tail, *m1, *v, *master, *w8,
-                                   *hp, skip, S(stream)));
+                                   *hp, skip, S(stream), w_hist, hist_slot));
   return FP8LM_OK;
 }
 

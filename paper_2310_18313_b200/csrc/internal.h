@@ -130,7 +130,8 @@ namespace fp8lm {
 enum ProfId : int {
   P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
   P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
-  P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_W8_BCAST, P_COUNT
+  P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_W8_BCAST, P_ADAM_DELAYED,
+  P_QADAM_DELAYED, P_COUNT
 };
 bool prof_on();
 struct ProfScope {
@@ -171,7 +172,14 @@ cudaError_t launch_adam_fused_local(const DevPlan& p, const void* grads, int src
                                    const float* s_g, uint8_t* g8, const TailArgs& tail,
                                    const fp8lm_stensors& m1, const fp8lm_stensors& v,
                                    const fp8lm_stensors& w, const fp8lm_stensors& w8,
-                                   const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s);
+                                   const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s,
+                                   float* w_hist = nullptr, int hist_slot = 0);
+// delayed state scaling: one AdamW pass (App. B)
+cudaError_t launch_adam_delayed(const DevPlan& p, const uint8_t* g8, const float* g_sinv,
+                                const fp8lm_stensors& m1, const fp8lm_stensors& v,
+                                const fp8lm_stensors& w, const fp8lm_stensors& w8,
+                                const fp8lm_adam_hp& hp, const int32_t* skip, float* w_hist,
+                                int hist_slot, cudaStream_t s);
 // mode P2P fused step: exchange + reduce + Adam pass 1 on the own shard (+ maxima exchange)
 cudaError_t launch_reduce_p2p_a1(const DevPlan& p, const P2PArgs& x, const float* s_g,
                                  const TailArgs& tail, uint8_t* g8, const fp8lm_stensors& m1,

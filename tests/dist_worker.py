@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--mode", choices=["nccl", "p2p", "zero"], default="nccl")
     ap.add_argument("--unfused", action="store_true",
                     help="the three ABI calls instead of fp8lm_dp_step")
+    ap.add_argument("--delayed", action="store_true", help="delayed state scaling (R25-R27)")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -72,9 +73,11 @@ def main():
     w0 = plan.flat(torch.float32)
     for t, v in enumerate(plan.views(w0)):
         synth.fill_weights(v, t)
-    dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr, fused=not args.unfused)
+    dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr, fused=not args.unfused,
+                           state_scaling="delayed" if args.delayed else "jit")
     ref_states = R.oracle_init(plan, w0)
     mus = [F32(1.0)] * plan.T
+    hists = [OA.init_history(st) for st in ref_states] if args.delayed else None
     ok = True
     msgs = []
     for step in range(1, args.steps + 1):
@@ -92,7 +95,10 @@ def main():
         gnp = [R.to_np_f32(g) for g in all_grads]
         per_rank = [[g[plan.offsets[t]: plan.offsets[t] + plan.numels[t]] for t in range(plan.T)]
                     for g in gnp]
-        res = OS.train_step(per_rank, mus, ref_states, OA.hyper_params(args.lr, step))
+        res = OS.train_step(per_rank, mus, ref_states, OA.hyper_params(args.lr, step), hists=hists,
+                            step=step)
+        if args.delayed:
+            hists = res["hists"]
         g8 = dp.g8.cpu().numpy() if args.mode != "zero" else None
         s_g = dp.s_g.cpu().numpy()
         sat = dp.sat.cpu().numpy()
@@ -139,7 +145,7 @@ def main():
     for m in msgs[:10]:
         print(m, flush=True)
     if rank == 0:
-        tag = args.mode.upper() + ("_UNFUSED" if args.unfused else "")
+        tag = args.mode.upper() + ("_UNFUSED" if args.unfused else "") + ("_DELAYED" if args.delayed else "")
         print(f"{tag} parity N={N}: {'OK' if flag.item() == 1 else 'MISMATCH'}", flush=True)
     comm.close()
     dist.destroy_process_group()

@@ -39,7 +39,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("mode", ["nccl", "p2p", "p2p_unfused", "zero"])
+@pytest.mark.parametrize("mode", ["nccl", "p2p", "p2p_unfused", "zero", "p2p_delayed", "zero_delayed"])
 @pytest.mark.parametrize("n", [2, 4])
 def test_multi_gpu_bit_exact(n, mode):
     if _ngpus() < n:
@@ -47,7 +47,8 @@ def test_multi_gpu_bit_exact(n, mode):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "dist_worker.py"), "--steps", "3",
-           "--mode", mode.replace("_unfused", "")] + (["--unfused"] if "unfused" in mode else [])
+           "--mode", mode.split("_")[0]] + (["--unfused"] if "unfused" in mode else []) + \
+          (["--delayed"] if "delayed" in mode else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"{mode.upper()} parity N={n}: OK" in r.stdout

@@ -89,7 +89,7 @@ RAGGED = [3, 16, 17, 64, 1000, 16384, 16385, 40000, 70001]
 
 
 def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float32,
-                     specials=None, amp=None, check_tensors=None, fused=True):
+                     specials=None, amp=None, check_tensors=None, fused=True, delayed=False):
     """Run the device path for `steps` steps and the oracle on the same inputs; compare
     every per-tensor output of every step.  check_tensors: oracle runs only on this
     subset (valid because nothing couples two tensors except the skip flag, and the
@@ -100,11 +100,13 @@ def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float3
     for t, v in enumerate(plan.views(w0)):
         if v.numel():
             synth.fill_weights(v, t)
-    dp = B.FP8DataParallel(plan, w0, lr=lr, fused=fused)
+    dp = B.FP8DataParallel(plan, w0, lr=lr, fused=fused,
+                           state_scaling="delayed" if delayed else "jit")
     sub = list(range(plan.T)) if check_tensors is None else list(check_tensors)
     ref_all = R.oracle_init(plan, w0)
     ref_states = [ref_all[t] for t in sub]
     mus = [F32(1.0)] * len(sub)
+    hists = [OA.init_history(st) for st in ref_states] if delayed else None
     torch.cuda.synchronize()
     for i, t in enumerate(sub):
         R.assert_state_equal(R.state_np(B, plan, dp.state, t), ref_states[i], f"init t={t}")
@@ -115,8 +117,14 @@ def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float3
         torch.cuda.synchronize()
         gnp = [R.to_np_f32(g) for g in grads]
         per_rank = [[g[plan.offsets[t]: plan.offsets[t] + plan.numels[t]] for t in sub] for g in gnp]
-        res = OS.train_step(per_rank, mus, ref_states, OA.hyper_params(lr, step))
+        res = OS.train_step(per_rank, mus, ref_states, OA.hyper_params(lr, step), hists=hists,
+                            step=step)
         assert bool(dp.skip.item()) == res["skip"], step
+        if delayed:
+            wh = dp.w_hist.cpu().numpy().reshape(16, -1)
+            for i, t in enumerate(sub):
+                assert np.array_equal(wh[:, t], res["hists"][i]), f"step {step} tensor {t}: history"
+            hists = res["hists"]
         amax = dp.amax.cpu().numpy().reshape(-1, max(plan.T, 1))
         s_g = dp.s_g.cpu().numpy()
         g8 = dp.g8.cpu().numpy()
@@ -216,6 +224,21 @@ def test_c2_full_set_sampled_tensors(B):
     numels = [s.numel for s in specs]
     pick = [0, 1, 2, 3, 4, 9, 10, len(specs) - 2, len(specs) - 1]
     _run_and_compare(B, numels, B.MODE_LOCAL, 1, steps=2, check_tensors=pick)
+
+
+@pytest.mark.parametrize("fused", [True, False], ids=["dp_step", "three_calls"])
+def test_delayed_scaling_local(B, fused):
+    """Delayed state scaling (App. B, R25-R27): one AdamW pass; 20 steps so the
+    16-slot amax(w) history wraps; fused (quantize + single pass) and separate calls."""
+    _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=20, fused=fused, delayed=True)
+
+
+def test_delayed_scaling_simulated_skip_bf16(B):
+    def specials(flat, r, step):
+        if step == 3 and r == 1:
+            flat[20] = float("nan")
+    _run_and_compare(B, RAGGED, B.MODE_SIMULATED, 2, steps=5, dtype=torch.bfloat16,
+                     specials=specials, delayed=True)
 
 
 def test_amax_screen_fallback_large_lr(B):
