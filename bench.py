@@ -54,30 +54,37 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grad-sets", type=int, default=0,
-                    help="independent gradient sets rotated step by step (0: 4 for GPT-125M, "
-                         "2 otherwise); a fixed gradient would drive every weight the same way")
+                    help="gradient sets rotated step by step, in antithetic pairs when even (0: 4 for "
+                         "GPT-125M, 2 for 7B, 1 for 13B)")
+    ap.add_argument("--state-scaling", default="jit", choices=["jit", "delayed"],
+                    help="optimizer-state scales: just-in-time (two AdamW passes, R19) or "
+                         "delayed from a 16-step amax history (one pass, R25-R27)")
     ap.add_argument("--quick", action="store_true",
                     help="profiling runs (ncu): no clock soak, no e2e, no cpu baseline")
     return ap.parse_args()
 
 
-def alg_bytes_per_param(N: int, zero: bool = False) -> float:
+def alg_bytes_per_param(N: int, zero: bool = False, delayed: bool = False) -> float:
     """A1 4 + A3 5 + A7 18 at N = 1 (A4/A5 identity); at N >= 2 add the
     reduce (1 + 1/N) and the all-gather write 2(N-1)/N.  ZeRO owner mode (C4): every rank
     reads its gradient twice (A1 4, A3 5), the owner reduce reads N x n/N codes and writes
     n/N (1 + 1/N), AdamW runs on n/N parameters (18/N) and the w8 broadcast reads n/N and
-    writes n (1/N + 1): 11 + 20/N."""
+    writes n (1/N + 1): 11 + 20/N.  Delayed state scaling (R25-R27) runs AdamW in one pass:
+    A7 = read g8 1 + m1 1 + v 2 + master 2, write m1 1 + v 2 + master 2 + w8 1 = 12."""
+    a7 = 12.0 if delayed else 18.0
     if zero:
-        return 11.0 + 20.0 / N
+        return 11.0 + (2.0 + a7) / N
     if N == 1:
-        return 27.0
-    return 28.0 + 1.0 / N + 2.0 * (N - 1) / N
+        return 9.0 + a7
+    return 10.0 + a7 + 1.0 / N + 2.0 * (N - 1) / N
 
 
 # per-launch algorithmic bytes per parameter of each kernel (LOCAL / NCCL modes)
 KERNEL_BYTES = {
     "amax": 4.0, "quantize": 5.0, "adam_pass1": 6.0, "adam_pass2": 12.0,
     "quantize+adam_pass1": 10.0,      # fused LOCAL kernel: read g 4, m1 1, v 2, master 2; write g8 1
+    "adam_delayed": 12.0,             # single pass: read g8 1, m1 1, v 2, master 2; write 6
+    "quantize+adam_delayed": 16.0,    # fused LOCAL: read g 4 + states 5; write g8 1 + states 5 + w8 1
 }
 
 
@@ -188,7 +195,9 @@ def oracle_sample(specs, config):
             if s.name.startswith("layer0.") and (len(s.shape) == 1 or s.name == "layer0.proj.w")]
 
 
-def run_oracle_step(specs, idx, rank, step, states):
+def run_oracle_step(specs, idx, rank, step, states, hists=None):
+    """One oracle step; hists (amax(w) rings) selects delayed state scaling.
+    Returns (seconds, states, hists)."""
     import numpy as np
     import torch
     import synth
@@ -200,8 +209,9 @@ def run_oracle_step(specs, idx, rank, step, states):
         synth.fill_gradient(g, 1, t, rank)
         grads.append(g.numpy())
     t0 = time.perf_counter()
-    res = OS.train_step([grads], [np.float32(1.0)] * len(idx), states, OA.hyper_params(6e-4, step))
-    return time.perf_counter() - t0, res["states"]
+    res = OS.train_step([grads], [np.float32(1.0)] * len(idx), states, OA.hyper_params(6e-4, step),
+                        hists=hists, step=step)
+    return time.perf_counter() - t0, res["states"], res["hists"]
 
 
 def oracle_states(specs, idx):
@@ -216,12 +226,17 @@ def oracle_states(specs, idx):
     return out
 
 
-def cpu_baseline(specs, config):
+def oracle_hists(states, delayed):
+    from oracle import adam as OA
+    return [OA.init_history(st) for st in states] if delayed else None
+
+
+def cpu_baseline(specs, config, delayed=False):
     idx = oracle_sample(specs, config)
     params = sum(specs[t].numel for t in idx)
     states = oracle_states(specs, idx)
-    dt, _ = run_oracle_step(specs, idx, 0, 1, states)
-    gbs = alg_bytes_per_param(1) * params / dt / 1e9
+    dt, _, _ = run_oracle_step(specs, idx, 0, 1, states, oracle_hists(states, delayed))
+    gbs = alg_bytes_per_param(1, delayed=delayed) * params / dt / 1e9
     return {"value": gbs, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{len(idx)} tensors ({params} params: {specs[idx[0]].name}..{specs[idx[-1]].name}) "
                       f"of {config}, one full step, N=1, numpy single-thread; {dt:.2f} s",
@@ -235,24 +250,26 @@ def run_reference(args, specs, world, rank):
     idx = oracle_sample(specs, args.config)
     params = sum(specs[t].numel for t in idx)
     states = oracle_states(specs, idx)
+    delayed = args.state_scaling == "delayed"
+    hists = oracle_hists(states, delayed)
     step = 0
     for _ in range(args.warmup):
         step += 1
-        _, states = run_oracle_step(specs, idx, 0, step, states)
+        _, states, hists = run_oracle_step(specs, idx, 0, step, states, hists)
     tot = 0.0
     for _ in range(args.steps):
         step += 1
-        dt, states = run_oracle_step(specs, idx, 0, step, states)
+        dt, states, hists = run_oracle_step(specs, idx, 0, step, states, hists)
         tot += dt
     ms = tot / args.steps * 1e3
-    value = alg_bytes_per_param(1) * params / (ms / 1e3) / 1e9
+    value = alg_bytes_per_param(1, delayed=delayed) * params / (ms / 1e3) / 1e9
     sample = (f"{len(idx)} tensors ({params} params) of {args.config} per step, N=1 math, "
               f"numpy single-thread")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config} gradient set, oracle sample", "tensors": len(idx),
-                       "params": params},
+                       "params": params, "state_scaling": args.state_scaling},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -287,14 +304,20 @@ def main():
     for t, v in enumerate(plan.views(w0)):
         synth.fill_weights(v, t)
     R = args.grad_sets or {"gpt-125m": 4, "gpt-7b": 2, "gpt-13b": 1}[args.config]
+    # antithetic rotation G1, -G1, G2, -G2, ...: a gradient with a persistent mean drives
+    # every weight to the sign-descent fixed point |w| = 1/wd within ~1e3 steps, a state
+    # no real run reaches (the weights pile up at amax(w) and crowd the amax screen)
     gsets = []
     for r_ in range(R):
         g = plan.flat(gdt)
         for t, v in enumerate(plan.views(g)):
-            synth.fill_gradient(v, 1 + r_, t, rank)
+            synth.fill_gradient(v, 1 + r_ // 2, t, rank)
+        if R % 2 == 0 and r_ % 2 == 1:
+            g.neg_()
         gsets.append(g)
     grads = gsets[0]
-    dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr)
+    delayed = args.state_scaling == "delayed"
+    dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr, state_scaling=args.state_scaling)
     del w0
     torch.cuda.synchronize()
     nstep = [0]
@@ -332,7 +355,7 @@ def main():
     ms_local = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms_local, world)
 
-    bytes_rank = alg_bytes_per_param(N, zero) * params
+    bytes_rank = alg_bytes_per_param(N, zero, delayed) * params
     if args.dtype == "bf16":
         bytes_rank -= 2.0 * 2 * params      # A1 and A3 read 2 B instead of 4
     value = N * bytes_rank / (ms / 1e3) / 1e9
@@ -360,7 +383,8 @@ def main():
         per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
         bpp = KERNEL_BYTES.get(dom)
         if bpp is not None:
-            if args.dtype == "bf16" and dom in ("amax", "quantize"):
+            if args.dtype == "bf16" and dom in ("amax", "quantize", "quantize+adam_pass1",
+                                                "quantize+adam_delayed"):
                 bpp -= 2.0
             np_ = kparams if dom.startswith("adam") else params
             achieved = bpp * np_ / (per_launch_ms / 1e3) / 1e9
@@ -409,7 +433,7 @@ def main():
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline and not args.quick:
-        cpu = cpu_baseline(specs, args.config)
+        cpu = cpu_baseline(specs, args.config, delayed)
 
     if rank == 0:
         line = {
@@ -421,10 +445,10 @@ def main():
                                    + (", ZeRO owner mode (Alg. 1)" if zero else ""),
                        "tensors": plan.T, "params": params, "grad_dtype": args.dtype,
                        "alg_bytes_per_param_per_rank": bytes_rank / params,
-                       "parallelism": f"dp{N}" if N > 1 else "single", "state_scaling": "jit",
+                       "parallelism": f"dp{N}" if N > 1 else "single", "state_scaling": args.state_scaling,
                        "exchange": (args.exchange if N > 1 else "none"),
                        "l2": "inputs larger than L2 (step moves %.2f GB/rank > 126 MB)" % (bytes_rank / 1e9),
-                       "grad_sets_rotated": R,
+                       "grad_sets_rotated": R, "grad_sets_antithetic": R % 2 == 0,
                        "hbm_frac_of_8tbs": value / N / 8000.0},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "kernels": breakdown,

@@ -206,6 +206,10 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
     items += (p->numel[t] + kChunk - 1) / kChunk;
   }
   p->item_start[T] = items;
+  p->items.reserve(items);
+  for (int t = 0; t < T; ++t)
+    for (int64_t x = 0; x < p->numel[t]; x += kChunk)
+      p->items.push_back(ShardItem{p->offset[t] + x, t, (int32_t)std::min<int64_t>(kChunk, p->numel[t] - x)});
   p->total = run;
   p->g8_bytes = run;
   if (dist) {
@@ -229,6 +233,7 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
   p->off_numel = take(sizeof(int64_t) * std::max(T, 1));
   p->off_offset = take(sizeof(int64_t) * std::max(T, 1));
   p->off_item_start = take(sizeof(int64_t) * (T + 1));
+  p->off_items = take(sizeof(ShardItem) * std::max<size_t>(p->items.size(), 1));
   p->off_shard_items = take(sizeof(ShardItem) * std::max<size_t>(p->shard_items.size(), 1));
   p->off_acc_amax = take(sizeof(uint32_t) * std::max(nsim * T, 1));
   p->off_acc_state = take(sizeof(uint32_t) * std::max(3 * T, 1));
@@ -404,6 +409,8 @@ int fp8lm_plan_bind(fp8lm_plan* p, void* ws, size_t ws_bytes, void* stream) {
     CUDA_TRY(cudaMemcpyAsync(b + p->off_offset, p->offset.data(), sizeof(int64_t) * p->T, cudaMemcpyHostToDevice, s));
   }
   CUDA_TRY(cudaMemcpyAsync(b + p->off_item_start, p->item_start.data(), sizeof(int64_t) * (p->T + 1), cudaMemcpyHostToDevice, s));
+  if (!p->items.empty())
+    CUDA_TRY(cudaMemcpyAsync(b + p->off_items, p->items.data(), sizeof(ShardItem) * p->items.size(), cudaMemcpyHostToDevice, s));
   if (!p->shard_items.empty())
     CUDA_TRY(cudaMemcpyAsync(b + p->off_shard_items, p->shard_items.data(), sizeof(ShardItem) * p->shard_items.size(), cudaMemcpyHostToDevice, s));
   // accumulators (acc_amax, acc_state, sat_part, sat_acc, counters: consecutive) zero at rest
@@ -417,6 +424,7 @@ int fp8lm_plan_bind(fp8lm_plan* p, void* ws, size_t ws_bytes, void* stream) {
   d.numel = reinterpret_cast<const int64_t*>(b + p->off_numel);
   d.offset = reinterpret_cast<const int64_t*>(b + p->off_offset);
   d.item_start = reinterpret_cast<const int64_t*>(b + p->off_item_start);
+  d.items = reinterpret_cast<const ShardItem*>(b + p->off_items);
   d.shard_items = reinterpret_cast<const ShardItem*>(b + p->off_shard_items);
   d.n_shard_items = (int64_t)p->shard_items.size();
   d.acc_amax = reinterpret_cast<uint32_t*>(b + p->off_acc_amax);

@@ -28,6 +28,7 @@ struct DevPlan {
   const int64_t* numel;     // [T]
   const int64_t* offset;    // [T]
   const int64_t* item_start;// [T+1]
+  const ShardItem* items;   // [n_items] full-tensor work items (pos, t, len): one 16-B load
   const ShardItem* shard_items;
   int64_t n_shard_items;
   uint32_t* acc_amax;       // [nsim*T]  float bits, atomicMax accumulators (zero at rest)
@@ -93,12 +94,12 @@ struct fp8lm_plan {
   int32_t nranks = 1;
   int32_t rank = 0;
   std::vector<int64_t> numel, offset, item_start;
-  std::vector<fp8lm::ShardItem> shard_items;
+  std::vector<fp8lm::ShardItem> items, shard_items;
   int64_t total = 0;        // elements per flat buffer
   int64_t shard = 0;        // S bytes (NCCL)
   int64_t g8_bytes = 0;
   // workspace layout (byte offsets)
-  size_t off_numel = 0, off_offset = 0, off_item_start = 0, off_shard_items = 0;
+  size_t off_numel = 0, off_offset = 0, off_item_start = 0, off_items = 0, off_shard_items = 0;
   size_t off_acc_amax = 0, off_acc_state = 0, off_sat_part = 0, off_sat_acc = 0, off_ctr = 0,
          off_acc_end = 0;
   size_t off_send = 0, off_recv = 0, off_sim = 0, ws_bytes = 0;
