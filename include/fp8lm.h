@@ -301,6 +301,49 @@ int fp8lm_prof_ids(void);
 int fp8lm_prof_read(int32_t id, const char** name, int64_t* launches, double* total_ms,
                     int32_t* is_ours);
 
+/* ------------------- (7) FP8 all-reduce strategies and Fig. 6 statistics (f3) */
+/* PAPER.md §2.1 P:102-121 compares three ways to aggregate FP8 gradients over N ranks:
+ * pre-scaling (Eq. 1, g = g_1/N + ... + g_N/N), post-scaling (Eq. 2, (g_1 + ... + g_N)/N)
+ * and automatic scaling (Eq. 3-6, the method); Fig. 6 reports their SNR,
+ * underflow rate and overflow rate.  Readings R28-R30:
+ *   s = Eq. 4's shared scale = fl(fl(448 / A) * mu), A = max over ranks and elements of
+ *       |g|, mu = *mu for AUTO and 1 for PRE / POST (1 if A = 0 or 448/A overflows)
+ *   PRE   c_r = E4M3(fl(fl(g_r * s) / N)), result scale s
+ *   POST  c_r = E4M3(fl(g_r * s)),          result scale fl(N * s)
+ *   AUTO  as POST with mu; *mu <- the mu update (R1-R3) from the result's saturation
+ *   then S = rank-order binary32 sum of decode(c_r), code = E4M3(S) (all three)
+ *   events = (N + 1) n encodes; underflow: nonzero input -> zero code; overflow: |input|
+ *   > 448; sig2 = sum m^2, err2 = sum (g_hat - m)^2 in binary64, m = binary64 rank-order
+ *   mean of g_r, g_hat = fl(decode(code) * fl(1 / result scale)); SNR = 10 log10(sig2/err2).
+ * grads: device, N rows of n binary32 values (row r = rank r), contiguous, any alignment.
+ * mu: device float[1], read by AUTO and replaced by the next step's mu (untouched by PRE
+ * and POST).  codes: device uint8[n] (the aggregated E4M3 codes) or NULL.  stats: device
+ * fp8lm_commstats, zero-initialised once by the caller; every call overwrites its
+ * outputs and returns its scratch fields to zero.  Non-finite gradients are not supported
+ * (s = 0: the statistics are then meaningless).  Asynchronous on `stream`; EINVAL on bad
+ * arguments (strategy, N < 1, n < 0, NULL pointers). */
+#define FP8LM_STRATEGY_PRE 0
+#define FP8LM_STRATEGY_POST 1
+#define FP8LM_STRATEGY_AUTO 2
+typedef struct {
+  double sig2;             /* sum over elements of m^2 */
+  double err2;             /* sum over elements of (g_hat - m)^2 */
+  uint64_t underflow;      /* encodes of a nonzero input that gave a zero code */
+  uint64_t overflow;       /* encodes whose input magnitude exceeded 448 */
+  uint64_t events;         /* (N + 1) * n */
+  uint32_t sat;            /* result codes attaining 448 (the mu statistic, R4) */
+  uint32_t nonfinite;      /* 1 if any input was inf / NaN */
+  float amax;              /* A */
+  float s;                 /* the shared scale used for the rank encodes */
+  float scale;             /* result scale (s for PRE, fl(N s) otherwise) */
+  float scale_inv;         /* fl(1 / scale) */
+  float mu_used;
+  float mu_next;
+  uint32_t scratch[4];     /* internal accumulators / tickets: zero at rest */
+} fp8lm_commstats;
+int fp8lm_allreduce_strategy(int32_t strategy, const float* grads, int32_t nranks, int64_t n,
+                             float* mu, uint8_t* codes, fp8lm_commstats* stats, void* stream);
+
 /* ----------------------------------------------------------- diagnostics (auxiliary) */
 /* Device self-test of the branch-free IEEE sqrt / division fast paths used by the
  * AdamW kernels: every non-negative binary32 input for sqrt, `div_pairs` seeded

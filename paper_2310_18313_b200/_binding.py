@@ -8,6 +8,8 @@ shared library is missing this module raises at import time.
 from __future__ import annotations
 
 import ctypes as C
+import math
+import struct
 import os
 from typing import List, Optional, Sequence
 
@@ -91,6 +93,7 @@ _sig("fp8lm_dp_step", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
      C.POINTER(AdamHP), _p, _i32, _p)
 _sig("fp8lm_adam_step_delayed", C.c_int, _p, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(STensors), C.POINTER(STensors), C.POINTER(AdamHP), _p, _p, _i32, _p)
+_sig("fp8lm_allreduce_strategy", C.c_int, _i32, _p, _i32, _i64, _p, _p, _p, _p)
 _sig("fp8lm_state_init", C.c_int, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(STensors), C.POINTER(STensors), _p)
 
@@ -370,6 +373,53 @@ def fp8_dequantize(codes: torch.Tensor, fmt: int, scale_inv: torch.Tensor, strea
     _check(lib.fp8lm_dequantize(_ptr(codes), fmt, codes.numel(), _ptr(scale_inv), _ptr(out),
                                 _stream(stream)), "fp8lm_dequantize")
     return out
+
+
+# ------------------------------------------------------------------ strategies (f3)
+STRATEGIES = {"pre": 0, "post": 1, "auto": 2}
+# fp8lm_commstats (include/fp8lm.h): 5 x 8-byte fields, 2 u32, 6 f32, 4 u32 scratch
+_COMMSTATS = struct.Struct("<ddQQQIIffffff4I")
+COMMSTATS_BYTES = _COMMSTATS.size
+
+
+def commstats_buffer(device) -> torch.Tensor:
+    """A zero-initialised device fp8lm_commstats (reuse it across calls)."""
+    return torch.zeros(COMMSTATS_BYTES // 8, dtype=torch.float64, device=device)
+
+
+def commstats_read(buf: torch.Tensor) -> dict:
+    """Host dict of one fp8lm_commstats (synchronises)."""
+    v = _COMMSTATS.unpack(buf.detach().cpu().numpy().tobytes())
+    keys = ("sig2", "err2", "underflow", "overflow", "events", "sat", "nonfinite", "amax", "s",
+            "scale", "scale_inv", "mu_used", "mu_next")
+    d = dict(zip(keys, v[:13]))
+    d["underflow_rate"] = d["underflow"] / d["events"] if d["events"] else 0.0
+    d["overflow_rate"] = d["overflow"] / d["events"] if d["events"] else 0.0
+    e, g = d["err2"], d["sig2"]
+    d["snr_db"] = (float("inf") if g > 0 else float("nan")) if e == 0 else (
+        10.0 * math.log10(g / e) if g > 0 else float("-inf"))
+    return d
+
+
+def allreduce_strategy(grads: torch.Tensor, strategy, mu: torch.Tensor = None,
+                       codes: torch.Tensor = None, stats: torch.Tensor = None, stream=None):
+    """fp8lm_allreduce_strategy: N ranks' gradients as rows of a [N, n] fp32 device tensor;
+    strategy "pre" | "post" | "auto" (Eq. 1 / Eq. 2 / Eq. 3-6).  Returns (codes, stats
+    buffer); read the statistics with commstats_read.  mu (device float[1]) is updated in
+    place by "auto"."""
+    st = STRATEGIES[strategy] if isinstance(strategy, str) else int(strategy)
+    assert grads.dim() == 2 and grads.dtype == torch.float32 and grads.is_contiguous()
+    N, n = grads.shape
+    dev = grads.device
+    if codes is None:
+        codes = torch.empty(n, dtype=torch.uint8, device=dev)
+    if stats is None:
+        stats = commstats_buffer(dev)
+    if st == 2 and mu is None:
+        raise ValueError("strategy auto needs mu")
+    _check(lib.fp8lm_allreduce_strategy(st, _ptr(grads), N, n, _ptr(mu), _ptr(codes), _ptr(stats),
+                                        _stream(stream)), "fp8lm_allreduce_strategy")
+    return codes, stats
 
 
 def _grads_arg(plan: Plan, grads):

@@ -4,6 +4,7 @@
 // file only validates arguments and enqueues work on the caller's stream.
 #include <algorithm>
 #include <cstdarg>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -525,6 +526,24 @@ int fp8lm_dequantize(const void* codes, int32_t fmt, int64_t n, const float* sca
     return fail(FP8LM_EINVAL, "dequantize: fmt must be E4M3, E5M2 or F16");
   if (n > 0 && (!codes || !dst || !scale_inv)) return fail(FP8LM_EINVAL, "dequantize: NULL pointer");
   CUDA_TRY(launch_dq_single(codes, fmt, n, scale_inv, dst, S(stream)));
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- (7) strategies (f3)
+static_assert(sizeof(fp8lm_commstats) == 88, "fp8lm_commstats layout (the binding unpacks 88 bytes)");
+static_assert(offsetof(fp8lm_commstats, sat) == 40 && offsetof(fp8lm_commstats, amax) == 48 &&
+              offsetof(fp8lm_commstats, scratch) == 72, "fp8lm_commstats layout");
+int fp8lm_allreduce_strategy(int32_t strategy, const float* grads, int32_t nranks, int64_t n,
+                             float* mu, uint8_t* codes, fp8lm_commstats* stats, void* stream) {
+  if (strategy < FP8LM_STRATEGY_PRE || strategy > FP8LM_STRATEGY_AUTO)
+    return fail(FP8LM_EINVAL, "allreduce_strategy: bad strategy %d", strategy);
+  if (nranks < 1) return fail(FP8LM_EINVAL, "allreduce_strategy: nranks must be >= 1");
+  if (n < 0) return fail(FP8LM_EINVAL, "allreduce_strategy: n < 0");
+  if (!stats) return fail(FP8LM_EINVAL, "allreduce_strategy: NULL stats");
+  if (n > 0 && !grads) return fail(FP8LM_EINVAL, "allreduce_strategy: NULL grads");
+  if (strategy == FP8LM_STRATEGY_AUTO && !mu) return fail(FP8LM_EINVAL, "allreduce_strategy: AUTO needs mu");
+  if (!aligned(stats, 8)) return fail(FP8LM_EINVAL, "allreduce_strategy: stats must be 8-byte aligned");
+  CUDA_TRY(launch_allreduce_strategy(strategy, grads, nranks, n, mu, codes, stats, S(stream)));
   return FP8LM_OK;
 }
 

@@ -132,7 +132,7 @@ enum ProfId : int {
   P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
   P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
   P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_W8_BCAST, P_ADAM_DELAYED,
-  P_QADAM_DELAYED, P_COUNT
+  P_QADAM_DELAYED, P_STRAT_AMAX, P_STRAT_REDUCE, P_COUNT
 };
 bool prof_on();
 struct ProfScope {
@@ -194,6 +194,8 @@ cudaError_t launch_state_init(const DevPlan& p, const float* w0, const fp8lm_ste
 cudaError_t launch_q_single(const void* src, int src_dtype, int64_t n, int fmt, void* dst,
                             float* scale, float* scale_inv, float* amax, int jit,
                             uint32_t* sat, cudaStream_t s);
+cudaError_t launch_allreduce_strategy(int strategy, const float* g, int N, int64_t n, float* mu,
+                                      uint8_t* codes, fp8lm_commstats* st, cudaStream_t s);
 cudaError_t launch_dq_single(const void* codes, int fmt, int64_t n, const float* scale_inv,
                              float* dst, cudaStream_t s);
 int num_sms();
