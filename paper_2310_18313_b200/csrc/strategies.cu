@@ -11,7 +11,7 @@
 //   k_strat_reduce  per element: the N rank encodes in rank order (pre: fl(fl(g s)/N)),
 //                   the binary32 rank-order sum, the encode of the sum, the dequantized
 //                   result against the binary64 mean; event counts and the two error
-//                   sums flush once per CTA; the last CTA runs the mu update (AUTO)
+//                   sums flush once per warp; the last CTA runs the mu update (AUTO)
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -130,59 +130,82 @@ struct Acc {
   uint32_t under = 0, over = 0, sat = 0;
 };
 
-// one encode event (R29): underflow = nonzero input -> zero code, overflow = |in| > 448
-__device__ __forceinline__ float enc_dec(float y, Acc& a, uint32_t& code) {
-  code = e4m3x2(y, 0.0f) & 0xFFu;
-  float d, unused;
-  dec_e4m3x2(code, d, unused);
-  a.under += (y != 0.0f) & (d == 0.0f);
-  a.over += fabsf(y) > 448.0f;
-  return d;
+// encode events (R29): underflow = nonzero input -> zero code, overflow = |in| > 448
+// (integer tests on the bit patterns: 448 = 0x43E00000; inputs are finite)
+__device__ __forceinline__ void count_events(float y, uint32_t code, Acc& a) {
+  const uint32_t ab = abs_bits(y);
+  a.under += (ab != 0u) & ((code & 0x7Fu) == 0u);
+  a.over += ab > 0x43E00000u;
+}
+
+// two encodes with one cvt each way: codes (lo byte = y0) and the exact decoded values
+__device__ __forceinline__ void enc_dec2(float y0, float y1, Acc& a, uint32_t& c0, uint32_t& c1,
+                                         float& d0, float& d1) {
+  const uint32_t c = e4m3x2(y0, y1);
+  dec_e4m3x2(c, d0, d1);
+  c0 = c & 0xFFu;
+  c1 = c >> 8;
+  count_events(y0, c0, a);
+  count_events(y1, c1, a);
 }
 
 template <int STRAT, int V>
 __device__ __forceinline__ void strat_elems(const float* __restrict__ g, int N, int64_t n, int64_t i,
                                             float s, float inv_n, bool pow2, float sinv,
                                             uint8_t* codes, Acc& a) {
-  float S[V];
-  double msum[V];
-#pragma unroll 2
+  constexpr int V2 = V < 2 ? 2 : V;       // V = 1 runs the pair code with a dummy lane
+  float S[V2];
+  double msum[V2];
+#pragma unroll 4
   for (int r = 0; r < N; ++r) {
-    float x[V];
+    float x[V2];
     if (V == 4) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(g + (int64_t)r * n + i));
       x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
     } else {
       x[0] = __ldg(g + (int64_t)r * n + i);
+      x[1] = 0.0f;
+    }
+    float y[V2];
+#pragma unroll
+    for (int j = 0; j < V2; ++j) {
+      y[j] = __fmul_rn(x[j], s);                                  // fl(g s)
+      if (STRAT == FP8LM_STRATEGY_PRE)                            // Eq. 1: fl(fl(g s) / N)
+        y[j] = pow2 ? __fmul_rn(y[j], inv_n) : __fdiv_rn(y[j], (float)N);
     }
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      float y = __fmul_rn(x[j], s);                               // fl(g s)
-      if (STRAT == FP8LM_STRATEGY_PRE)                            // Eq. 1: fl(fl(g s) / N)
-        y = pow2 ? __fmul_rn(y, inv_n) : __fdiv_rn(y, (float)N);
-      uint32_t c;
-      const float d = enc_dec(y, a, c);
+    for (int j = 0; j < V2; j += 2) {
+      uint32_t c0, c1;
+      float d0, d1;
+      enc_dec2(y[j], y[j + 1], a, c0, c1, d0, d1);
       if (r == 0) {                                               // rank order (R12)
-        S[j] = d;
-        msum[j] = (double)x[j];
+        S[j] = d0; S[j + 1] = d1;
+        msum[j] = (double)x[j]; msum[j + 1] = (double)x[j + 1];
       } else {
-        S[j] = __fadd_rn(S[j], d);
+        S[j] = __fadd_rn(S[j], d0); S[j + 1] = __fadd_rn(S[j + 1], d1);
         msum[j] = __dadd_rn(msum[j], (double)x[j]);
+        msum[j + 1] = __dadd_rn(msum[j + 1], (double)x[j + 1]);
       }
     }
   }
   uint32_t cw = 0;
 #pragma unroll
-  for (int j = 0; j < V; ++j) {
-    uint32_t c;
-    const float d = enc_dec(S[j], a, c);                          // E4M3 of the sum (R13)
-    a.sat += (c & 0x7Fu) == 0x7Eu;
-    const float gh = __fmul_rn(d, sinv);                          // A6 dequantize
-    const double m = __ddiv_rn(msum[j], (double)N);
-    const double e = __dsub_rn((double)gh, m);
-    a.sig2 = __fma_rn(m, m, a.sig2);
-    a.err2 = __fma_rn(e, e, a.err2);
-    cw |= c << (8 * j);
+  for (int j = 0; j < V2; j += 2) {
+    uint32_t c0, c1;
+    float d0, d1;
+    enc_dec2(S[j], S[j + 1], a, c0, c1, d0, d1);   // E4M3 of the sum (R13); a dummy lane is 0
+    const uint32_t cc[2] = {c0, c1};
+    const float dd[2] = {d0, d1};
+#pragma unroll
+    for (int h = 0; h < (V == 1 ? 1 : 2); ++h) {
+      a.sat += (cc[h] & 0x7Fu) == 0x7Eu;
+      const float gh = __fmul_rn(dd[h], sinv);                    // A6 dequantize
+      const double m = __ddiv_rn(msum[j + h], (double)N);
+      const double e = __dsub_rn((double)gh, m);
+      a.sig2 = __fma_rn(m, m, a.sig2);
+      a.err2 = __fma_rn(e, e, a.err2);
+      cw |= cc[h] << (8 * (j + h));
+    }
   }
   if (codes) {
     if (V == 4) *reinterpret_cast<uint32_t*>(codes + i) = cw;
