@@ -344,6 +344,45 @@ typedef struct {
 int fp8lm_allreduce_strategy(int32_t strategy, const float* grads, int32_t nranks, int64_t n,
                              float* mu, uint8_t* codes, fp8lm_commstats* stats, void* stream);
 
+/* ------------------ (8) FP8 sequence/tensor-parallel activation converter g (f4) */
+/* PAPER.md §2.3, Fig. 5: "We add an FP8 datatype conversion prior to g, such
+ * that the all-gather (or reduce-scatter) operation uses FP8 low-bit activation to save
+ * communication cost across GPUs."  Readings R31-R32:
+ *   s = Eq. 4's shared scale over the ranks' inputs, mu = 1: min_r fl(448 / amax_r)
+ *       (+inf for all-zero ranks; 1 if every rank is zero; 0 if any input is inf/NaN)
+ *   all-gather (forward):  rank r holds x_r (m elements); every rank receives the
+ *       gathered codes E4M3(fl(x_r * s)), rank-major (N m bytes), scale s;
+ *       out = fl(decode(code) * fl(1/s)) in out_dtype (bf16: round-to-nearest-even)
+ *   reduce-scatter (backward): rank r holds dy_r (N m elements); every rank quantizes
+ *       E4M3(fl(dy_r * s)); rank k receives S = rank-order binary32 sum of chunk k of
+ *       every rank's codes, out = fl(S * fl(1/s)) (no requantization, no mu)
+ * Transport: NVLink peer memory between the ranks of `comm` (CUDA IPC windows owned by
+ * the fp8lm_sp object), no NCCL call on the data path; 1 B per element crosses NVLink
+ * instead of 2 for bf16.  Every call is COLLECTIVE: all ranks call the same sequence of
+ * ops with the same m (ops are matched by a per-object counter), asynchronous on
+ * `stream`; a rank that never arrives makes the others trap after 20 s.
+ *
+ * fp8lm_sp_create: collective over comm (NULL = a single rank, no peers); max_elems
+ * bounds N*m of every later op.  Allocates two windows of max_elems bytes and a 512-byte
+ * pad per rank, exchanges IPC handles (ncclAllGather on `stream`, synchronised).  EINVAL
+ * on bad arguments, ECUDA / ENCCL on failure.  fp8lm_sp_destroy: unmaps and frees.
+ * fp8lm_sp_allgather: x (device, x_dtype F32 or BF16, m elements); codes_out (device
+ * uint8[N m] or NULL); out (device [N m] of out_dtype F32 or BF16, or NULL); scale_out
+ * (device float[2]: s, fl(1/s), or NULL).  The op is complete for this rank's readers
+ * when the stream reaches its end (the kernels wait for every peer's data).
+ * fp8lm_sp_reduce_scatter: dy (device, dtype F32 or BF16, N m elements: the full
+ * tensor, chunk k = elements [k m, (k+1) m)); out (device [m] of out_dtype) receives
+ * this rank's chunk of the sum; scale_out as above.
+ * Sizes with m % 16 == 0 and 32-byte aligned inputs take the vector kernels; others
+ * are correct but slower. */
+typedef struct fp8lm_sp fp8lm_sp;   /* opaque */
+int fp8lm_sp_create(fp8lm_comm* comm, int64_t max_elems, void* stream, fp8lm_sp** out);
+int fp8lm_sp_destroy(fp8lm_sp* sp);
+int fp8lm_sp_allgather(fp8lm_sp* sp, const void* x, int32_t x_dtype, int64_t m, uint8_t* codes_out,
+                       void* out, int32_t out_dtype, float* scale_out, void* stream);
+int fp8lm_sp_reduce_scatter(fp8lm_sp* sp, const void* dy, int32_t dtype, int64_t m, void* out,
+                            int32_t out_dtype, float* scale_out, void* stream);
+
 /* ----------------------------------------------------------- diagnostics (auxiliary) */
 /* Device self-test of the branch-free IEEE sqrt / division fast paths used by the
  * AdamW kernels: every non-negative binary32 input for sqrt, `div_pairs` seeded

@@ -93,6 +93,10 @@ _sig("fp8lm_dp_step", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
      C.POINTER(AdamHP), _p, _i32, _p)
 _sig("fp8lm_adam_step_delayed", C.c_int, _p, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(STensors), C.POINTER(STensors), C.POINTER(AdamHP), _p, _p, _i32, _p)
+_sig("fp8lm_sp_create", C.c_int, _p, _i64, _p, C.POINTER(_p))
+_sig("fp8lm_sp_destroy", C.c_int, _p)
+_sig("fp8lm_sp_allgather", C.c_int, _p, _p, _i32, _i64, _p, _p, _i32, _p, _p)
+_sig("fp8lm_sp_reduce_scatter", C.c_int, _p, _p, _i32, _i64, _p, _i32, _p, _p)
 _sig("fp8lm_allreduce_strategy", C.c_int, _i32, _p, _i32, _i64, _p, _p, _p, _p)
 _sig("fp8lm_state_init", C.c_int, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(STensors), C.POINTER(STensors), _p)
@@ -373,6 +377,63 @@ def fp8_dequantize(codes: torch.Tensor, fmt: int, scale_inv: torch.Tensor, strea
     _check(lib.fp8lm_dequantize(_ptr(codes), fmt, codes.numel(), _ptr(scale_inv), _ptr(out),
                                 _stream(stream)), "fp8lm_dequantize")
     return out
+
+
+# ------------------------------------------------------------------ SP converter (f4)
+class SPConverter:
+    """FP8 activation converter g between the sequence- and tensor-parallel regions
+    (§2.3, Fig. 5): all-gather (forward) and reduce-scatter (backward) of activations in
+    E4M3 over NVLink peer memory (fp8lm_sp_*).  comm=None: a single rank."""
+
+    def __init__(self, max_elems: int, comm: Optional[Comm] = None, device=None, stream=None):
+        self.nranks = comm.nranks if comm is not None else 1
+        self.rank = comm.rank if comm is not None else 0
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        h = _p()
+        _check(lib.fp8lm_sp_create(comm.handle if comm is not None else None, int(max_elems),
+                                   _stream(stream), C.byref(h)), "fp8lm_sp_create")
+        self.handle = h
+        self.scale = torch.ones(2, dtype=torch.float32, device=self.device)
+
+    def allgather(self, x: torch.Tensor, out_dtype=torch.bfloat16, codes: bool = False,
+                  out: torch.Tensor = None, codes_out: torch.Tensor = None, stream=None):
+        """x: this rank's partition (fp32 / bf16, m elements).  Returns (out [N m] of
+        out_dtype or None, codes [N m] uint8 or None); self.scale = (s, 1/s)."""
+        x = x.contiguous()
+        m = x.numel()
+        if out is None and out_dtype is not None:
+            out = torch.empty(self.nranks * m, dtype=out_dtype, device=x.device)
+        if codes and codes_out is None:
+            codes_out = torch.empty(self.nranks * m, dtype=torch.uint8, device=x.device)
+        _check(lib.fp8lm_sp_allgather(self.handle, _ptr(x), _dtype_code(x), m, _ptr(codes_out), _ptr(out),
+                                      _dtype_code(out) if out is not None else F32, _ptr(self.scale),
+                                      _stream(stream)), "fp8lm_sp_allgather")
+        return out, codes_out
+
+    def reduce_scatter(self, dy: torch.Tensor, out_dtype=torch.bfloat16, out: torch.Tensor = None,
+                       stream=None):
+        """dy: this rank's full gradient (N m elements).  Returns this rank's chunk [m] of
+        the sum, in out_dtype."""
+        dy = dy.contiguous()
+        assert dy.numel() % self.nranks == 0
+        m = dy.numel() // self.nranks
+        if out is None:
+            out = torch.empty(m, dtype=out_dtype, device=dy.device)
+        _check(lib.fp8lm_sp_reduce_scatter(self.handle, _ptr(dy), _dtype_code(dy), m, _ptr(out),
+                                           _dtype_code(out), _ptr(self.scale), _stream(stream)),
+               "fp8lm_sp_reduce_scatter")
+        return out
+
+    def close(self):
+        if self.handle:
+            lib.fp8lm_sp_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------ strategies (f3)

@@ -529,6 +529,133 @@ int fp8lm_dequantize(const void* codes, int32_t fmt, int64_t n, const float* sca
   return FP8LM_OK;
 }
 
+// ---------------------------------------------------------------- (8) FP8 SP converter (f4)
+struct fp8lm_sp {
+  int32_t nranks = 1, rank = 0;
+  int64_t max_elems = 0;
+  uint8_t* recv = nullptr;
+  uint8_t* send = nullptr;
+  uint32_t* pad = nullptr;
+  uint32_t* scratch = nullptr;
+  std::vector<void*> mapped;
+  uint32_t epoch = 0;
+};
+
+int fp8lm_sp_create(fp8lm_comm* comm, int64_t max_elems, void* stream, fp8lm_sp** out) {
+  if (!out) return fail(FP8LM_EINVAL, "sp_create: NULL out");
+  *out = nullptr;
+  if (max_elems < 0) return fail(FP8LM_EINVAL, "sp_create: max_elems < 0");
+  const int N = comm ? comm->nranks : 1;
+  const int rank = comm ? comm->rank : 0;
+  if (N > FP8LM_MAX_P2P_RANKS) return fail(FP8LM_EINVAL, "sp_create: at most %d ranks", FP8LM_MAX_P2P_RANKS);
+  auto* sp = new fp8lm_sp();
+  sp->nranks = N;
+  sp->rank = rank;
+  sp->max_elems = max_elems;
+  const size_t win = (size_t)std::max<int64_t>(round_up(max_elems, 256), 256);
+  auto bail = [&](int rc) { fp8lm_sp_destroy(sp); return rc; };
+  if (cudaMalloc(&sp->recv, win) != cudaSuccess || cudaMalloc(&sp->send, win) != cudaSuccess ||
+      cudaMalloc(&sp->pad, kSpPadBytes) != cudaSuccess ||
+      cudaMalloc(&sp->scratch, sizeof(uint32_t) * kSpScrWords) != cudaSuccess)
+    return bail(fail(FP8LM_ECUDA, "sp_create: cudaMalloc failed"));
+  if (cudaMemset(sp->pad, 0, kSpPadBytes) != cudaSuccess ||
+      cudaMemset(sp->scratch, 0, sizeof(uint32_t) * kSpScrWords) != cudaSuccess)
+    return bail(fail(FP8LM_ECUDA, "sp_create: cudaMemset failed"));
+  SpTable tab{};
+  tab.recv[rank] = sp->recv;
+  tab.send[rank] = sp->send;
+  tab.pad[rank] = sp->pad;
+  if (N > 1) {
+#ifdef FP8LM_WITH_NCCL
+    struct Handles { cudaIpcMemHandle_t recv, send, pad; };
+    Handles mine;
+    if (cudaIpcGetMemHandle(&mine.recv, sp->recv) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.send, sp->send) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.pad, sp->pad) != cudaSuccess)
+      return bail(fail(FP8LM_ECUDA, "sp_create: cudaIpcGetMemHandle failed"));
+    Handles* dev = nullptr;
+    if (cudaMalloc(&dev, sizeof(Handles) * N) != cudaSuccess)
+      return bail(fail(FP8LM_ECUDA, "sp_create: cudaMalloc failed"));
+    cudaMemcpy(dev + rank, &mine, sizeof(Handles), cudaMemcpyHostToDevice);
+    cudaStream_t s = S(stream);
+    const ncclResult_t nr = ncclAllGather(dev + rank, dev, sizeof(Handles), ncclUint8, comm->comm, s);
+    std::vector<Handles> all(N);
+    const cudaError_t ce = cudaStreamSynchronize(s);
+    cudaMemcpy(all.data(), dev, sizeof(Handles) * N, cudaMemcpyDeviceToHost);
+    cudaFree(dev);
+    if (nr != ncclSuccess || ce != cudaSuccess) return bail(fail(FP8LM_ENCCL, "sp_create: handle exchange failed"));
+    for (int q = 0; q < N; ++q) {
+      if (q == rank) continue;
+      void *pr = nullptr, *ps = nullptr, *pp = nullptr;
+      if (cudaIpcOpenMemHandle(&pr, all[q].recv, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+          cudaIpcOpenMemHandle(&ps, all[q].send, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+          cudaIpcOpenMemHandle(&pp, all[q].pad, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return bail(fail(FP8LM_ECUDA, "sp_create: cudaIpcOpenMemHandle failed"));
+      sp->mapped.push_back(pr);
+      sp->mapped.push_back(ps);
+      sp->mapped.push_back(pp);
+      tab.recv[q] = static_cast<uint8_t*>(pr);
+      tab.send[q] = static_cast<uint8_t*>(ps);
+      tab.pad[q] = static_cast<uint32_t*>(pp);
+    }
+#else
+    (void)stream;
+    return bail(fail(FP8LM_EUNSUPPORTED, "sp_create: built without NCCL"));
+#endif
+  }
+  if (cudaMemcpy(reinterpret_cast<uint8_t*>(sp->pad) + kSpPadTable, &tab, sizeof tab,
+                 cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(fail(FP8LM_ECUDA, "sp_create: table upload failed"));
+  *out = sp;
+  return FP8LM_OK;
+}
+
+int fp8lm_sp_destroy(fp8lm_sp* sp) {
+  if (!sp) return FP8LM_OK;
+  for (void* m : sp->mapped) cudaIpcCloseMemHandle(m);
+  if (sp->recv) cudaFree(sp->recv);
+  if (sp->send) cudaFree(sp->send);
+  if (sp->pad) cudaFree(sp->pad);
+  if (sp->scratch) cudaFree(sp->scratch);
+  delete sp;
+  return FP8LM_OK;
+}
+
+static int sp_check(const fp8lm_sp* sp, const void* src, int32_t dtype, int64_t m, const void* out,
+                    int32_t out_dtype, const char* who) {
+  if (!sp) return fail(FP8LM_EINVAL, "%s: sp is NULL", who);
+  if (m < 0) return fail(FP8LM_EINVAL, "%s: m < 0", who);
+  if (m * sp->nranks > sp->max_elems)
+    return fail(FP8LM_EINVAL, "%s: N*m = %lld exceeds max_elems %lld", who, (long long)(m * sp->nranks),
+                (long long)sp->max_elems);
+  if (dtype != FP8LM_F32 && dtype != FP8LM_BF16) return fail(FP8LM_EUNSUPPORTED, "%s: input must be F32 or BF16", who);
+  if (out && out_dtype != FP8LM_F32 && out_dtype != FP8LM_BF16)
+    return fail(FP8LM_EUNSUPPORTED, "%s: output must be F32 or BF16", who);
+  if (m > 0 && !src) return fail(FP8LM_EINVAL, "%s: NULL input", who);
+  return FP8LM_OK;
+}
+
+int fp8lm_sp_allgather(fp8lm_sp* sp, const void* x, int32_t x_dtype, int64_t m, uint8_t* codes_out,
+                       void* out, int32_t out_dtype, float* scale_out, void* stream) {
+  int rc = sp_check(sp, x, x_dtype, m, out, out_dtype, "sp_allgather");
+  if (rc) return rc;
+  SpArgs a{sp->pad, sp->scratch, sp->rank, sp->nranks, ++sp->epoch, false};
+  a.vec = m % 16 == 0 && aligned(x, 32) && (!codes_out || aligned(codes_out, 16));
+  CUDA_TRY(launch_sp_allgather(x, x_dtype, m, codes_out, out, out_dtype, scale_out, a, S(stream)));
+  return FP8LM_OK;
+}
+
+int fp8lm_sp_reduce_scatter(fp8lm_sp* sp, const void* dy, int32_t dtype, int64_t m, void* out,
+                            int32_t out_dtype, float* scale_out, void* stream) {
+  int rc = sp_check(sp, dy, dtype, m, out, out_dtype, "sp_reduce_scatter");
+  if (rc) return rc;
+  if (m > 0 && !out) return fail(FP8LM_EINVAL, "sp_reduce_scatter: NULL out");
+  SpArgs a{sp->pad, sp->scratch, sp->rank, sp->nranks, ++sp->epoch, false};
+  a.vec = m % 16 == 0 && aligned(dy, 32);
+  CUDA_TRY(launch_sp_reduce_scatter(dy, dtype, m, out, out_dtype, scale_out, a, S(stream)));
+  return FP8LM_OK;
+}
+
 // ---------------------------------------------------------------- (7) strategies (f3)
 static_assert(sizeof(fp8lm_commstats) == 88, "fp8lm_commstats layout (the binding unpacks 88 bytes)");
 static_assert(offsetof(fp8lm_commstats, sat) == 40 && offsetof(fp8lm_commstats, amax) == 48 &&

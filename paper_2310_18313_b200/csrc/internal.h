@@ -76,6 +76,29 @@ struct P2PArgs {
   uint32_t epoch;         // step counter: flags hold the epoch of their last signal
 };
 
+// ---------------------------------------------------------------- FP8 SP converter (f4)
+// pad of one rank (bytes): three flag rows (one u32 epoch per source rank), the ranks'
+// local scales, then the peer table
+constexpr size_t kSpPadFlagScale = 0, kSpPadFlagData = 64, kSpPadFlagDone = 128, kSpPadScales = 192,
+                 kSpPadTable = 256, kSpPadBytes = 512;
+struct SpTable {
+  uint8_t* recv[kMaxPeers];   // all-gather receive windows (N m bytes)
+  uint8_t* send[kMaxPeers];   // reduce-scatter send windows (N m bytes)
+  uint32_t* pad[kMaxPeers];
+};
+static_assert(kSpPadTable + sizeof(SpTable) <= kSpPadBytes, "sp pad layout");
+// local scratch (u32 words, zero at rest except s / sinv)
+constexpr int kSpScrAmax = 0, kSpScrBad = 1, kSpScrTicketA = 2, kSpScrTicketB = 3, kSpScrTicketC = 4,
+              kSpScrS = 5, kSpScrSinv = 6, kSpScrWords = 8;
+struct SpArgs {
+  uint32_t* pad;       // this rank's pad (its table copy at kSpPadTable)
+  uint32_t* scratch;
+  int rank;
+  int nranks;
+  uint32_t epoch;
+  bool vec;            // 16-element vector paths (sizes multiples of 16, aligned buffers)
+};
+
 // outputs of the Eq. 6 / mu tail of fp8lm_grad_allreduce
 struct TailArgs {
   int nranks;
@@ -132,7 +155,8 @@ enum ProfId : int {
   P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
   P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
   P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_W8_BCAST, P_ADAM_DELAYED,
-  P_QADAM_DELAYED, P_STRAT_AMAX, P_STRAT_REDUCE, P_COUNT
+  P_QADAM_DELAYED, P_STRAT_AMAX, P_STRAT_REDUCE, P_SP_AMAX, P_SP_PUSH, P_SP_GATHER, P_SP_QUANT,
+  P_SP_PULL, P_COUNT
 };
 bool prof_on();
 struct ProfScope {
@@ -196,6 +220,10 @@ cudaError_t launch_q_single(const void* src, int src_dtype, int64_t n, int fmt, 
                             uint32_t* sat, cudaStream_t s);
 cudaError_t launch_allreduce_strategy(int strategy, const float* g, int N, int64_t n, float* mu,
                                       uint8_t* codes, fp8lm_commstats* st, cudaStream_t s);
+cudaError_t launch_sp_allgather(const void* x, int x_dtype, int64_t m, uint8_t* codes_out, void* out,
+                                int out_dtype, float* scale_out, const SpArgs& a, cudaStream_t s);
+cudaError_t launch_sp_reduce_scatter(const void* dy, int dtype, int64_t m, void* out, int out_dtype,
+                                     float* scale_out, const SpArgs& a, cudaStream_t s);
 cudaError_t launch_dq_single(const void* codes, int fmt, int64_t n, const float* scale_inv,
                              float* dst, cudaStream_t s);
 int num_sms();
