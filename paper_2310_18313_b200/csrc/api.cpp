@@ -640,7 +640,8 @@ int fp8lm_sp_allgather(fp8lm_sp* sp, const void* x, int32_t x_dtype, int64_t m, 
   int rc = sp_check(sp, x, x_dtype, m, out, out_dtype, "sp_allgather");
   if (rc) return rc;
   SpArgs a{sp->pad, sp->scratch, sp->rank, sp->nranks, ++sp->epoch, false};
-  a.vec = m % 16 == 0 && aligned(x, 32) && (!codes_out || aligned(codes_out, 16));
+  a.vec = m % 16 == 0 && aligned(x, 32) && (!codes_out || aligned(codes_out, 16)) &&
+          (!out || aligned(out, 16));
   CUDA_TRY(launch_sp_allgather(x, x_dtype, m, codes_out, out, out_dtype, scale_out, a, S(stream)));
   return FP8LM_OK;
 }
@@ -651,7 +652,7 @@ int fp8lm_sp_reduce_scatter(fp8lm_sp* sp, const void* dy, int32_t dtype, int64_t
   if (rc) return rc;
   if (m > 0 && !out) return fail(FP8LM_EINVAL, "sp_reduce_scatter: NULL out");
   SpArgs a{sp->pad, sp->scratch, sp->rank, sp->nranks, ++sp->epoch, false};
-  a.vec = m % 16 == 0 && aligned(dy, 32);
+  a.vec = m % 16 == 0 && aligned(dy, 32) && aligned(out, 16);
   CUDA_TRY(launch_sp_reduce_scatter(dy, dtype, m, out, out_dtype, scale_out, a, S(stream)));
   return FP8LM_OK;
 }

@@ -89,7 +89,7 @@ struct SpTable {
 static_assert(kSpPadTable + sizeof(SpTable) <= kSpPadBytes, "sp pad layout");
 // local scratch (u32 words, zero at rest except s / sinv)
 constexpr int kSpScrAmax = 0, kSpScrBad = 1, kSpScrTicketA = 2, kSpScrTicketB = 3, kSpScrTicketC = 4,
-              kSpScrS = 5, kSpScrSinv = 6, kSpScrWords = 8;
+              kSpScrS = 5, kSpScrSinv = 6, kSpScrFlag1 = 7, kSpScrFlag2 = 8, kSpScrWords = 16;
 struct SpArgs {
   uint32_t* pad;       // this rank's pad (its table copy at kSpPadTable)
   uint32_t* scratch;
@@ -155,8 +155,7 @@ enum ProfId : int {
   P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
   P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
   P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_W8_BCAST, P_ADAM_DELAYED,
-  P_QADAM_DELAYED, P_STRAT_AMAX, P_STRAT_REDUCE, P_SP_AMAX, P_SP_PUSH, P_SP_GATHER, P_SP_QUANT,
-  P_SP_PULL, P_COUNT
+  P_QADAM_DELAYED, P_STRAT_AMAX, P_STRAT_REDUCE, P_SP_ALLGATHER, P_SP_REDUCE_SCATTER, P_COUNT
 };
 bool prof_on();
 struct ProfScope {

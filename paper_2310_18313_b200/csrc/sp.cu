@@ -4,17 +4,16 @@
 // reduce-scatter) operation uses FP8 low-bit activation to save communication cost".
 //
 // Transport: NVLink peer memory (CUDA IPC windows of fp8lm_sp), no NCCL on the data
-// path.  Every op is three kernels on the caller's stream:
-//   k_sp_amax        local amax -> s_r; the last CTA publishes s_r into every rank's pad,
-//                    waits for all ranks and takes the MIN (Eq. 4)
-//   all-gather:      k_sp_push      quantize the local partition and STORE the codes into
-//                                   every rank's receive window (push all-gather)
-//                    k_sp_gather    wait for every rank's data, copy the gathered codes
-//                                   and / or dequantize them into the caller's buffers
-//   reduce-scatter:  k_sp_quant     quantize the full local gradient into the own send
-//                                   window
-//                    k_sp_pull      wait, LOAD chunk `rank` from every rank's send window,
-//                                   rank-order binary32 sum, fl(S * fl(1/s)) -> out
+// path.  Every op is ONE cooperative kernel in three phases separated by grid barriers:
+//   1  local amax -> s_r; the last CTA publishes s_r into every rank's pad, waits for all
+//      ranks and takes the MIN (Eq. 4)
+//   2  all-gather: quantize the local partition and STORE the codes into every rank's
+//      receive window (push); reduce-scatter: quantize the full local gradient into the
+//      own send window; the last CTA releases "data" to every rank, all CTAs wait for
+//      every rank's "data"
+//   3  all-gather: copy the gathered codes and / or dequantize them into the caller's
+//      buffers; reduce-scatter: LOAD chunk `rank` from every rank's send window, sum in
+//      rank order in binary32, fl(S * fl(1/s)) -> out
 // Flags carry the op's epoch (host counter, identical on every rank): "scale" (s_r
 // published), "data" (codes stored / quantized) and "done" (this rank no longer reads
 // its receive window / peers' send windows for that epoch), each one u32 per source
@@ -22,7 +21,9 @@
 // of every rank before overwriting a window somebody may still read.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "internal.h"
@@ -62,9 +63,11 @@ __device__ __forceinline__ Peers<NR> load_peers(const SpArgs& a) {
   return P;
 }
 
-__device__ __forceinline__ bool sp_last_cta(uint32_t* ticket) {
+// sys: this CTA wrote memory that peers read (peer stores, the own send window)
+__device__ __forceinline__ bool sp_last_cta(uint32_t* ticket, bool sys) {
   __shared__ int last;
-  __threadfence_system();       // this CTA's peer stores / local writes
+  if (sys) __threadfence_system();
+  else __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t t = atomicAdd(ticket, 1u);
@@ -72,7 +75,10 @@ __device__ __forceinline__ bool sp_last_cta(uint32_t* ticket) {
     if (last) *ticket = 0;
   }
   __syncthreads();
-  if (last) __threadfence_system();
+  if (last) {
+    if (sys) __threadfence_system();
+    else __threadfence();
+  }
   return last;
 }
 
@@ -106,13 +112,65 @@ template <> struct In<__nv_bfloat16> {
   }
 };
 
-// ------------------------------------------------------------------ A, s_r, MIN
+template <typename O> struct Out;
+template <> struct Out<float> {
+  static __device__ __forceinline__ void put(float* p, int64_t i, float v) { p[i] = v; }
+  static __device__ __forceinline__ void put16(float* p, int64_t i, const float* v) {
+#pragma unroll
+    for (int k = 0; k < 16; k += 4)
+      st128(p + i + k, make_uint4(__float_as_uint(v[k]), __float_as_uint(v[k + 1]),
+                                  __float_as_uint(v[k + 2]), __float_as_uint(v[k + 3])));
+  }
+};
+template <> struct Out<__nv_bfloat16> {
+  static __device__ __forceinline__ void put(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
+  static __device__ __forceinline__ uint32_t pack(float lo, float hi) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);     // RNE, lo in the low half
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ void put16(__nv_bfloat16* p, int64_t i, const float* v) {
+    st128(p + i, make_uint4(pack(v[0], v[1]), pack(v[2], v[3]), pack(v[4], v[5]), pack(v[6], v[7])));
+    st128(p + i + 8, make_uint4(pack(v[8], v[9]), pack(v[10], v[11]), pack(v[12], v[13]), pack(v[14], v[15])));
+  }
+};
+
+// grid-wide barrier of a cooperative launch: the last CTA to arrive runs `last` (thread
+// 0), then releases the others through a local flag holding the op's epoch
+template <typename F>
+__device__ __forceinline__ void grid_phase(const SpArgs& a, int ticket, int flag, bool sys, F&& last) {
+  if (sp_last_cta(a.scratch + ticket, sys)) {
+    if (threadIdx.x == 0) {
+      last();
+      __threadfence();
+      atomicExch(a.scratch + flag, a.epoch);
+    }
+  }
+  if (threadIdx.x == 0) {
+    volatile uint32_t* f = a.scratch + flag;
+    while (*f != a.epoch) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ phase 1: A, s_r, MIN
 template <typename T, int NR>
-__global__ void __launch_bounds__(kSpT) k_sp_amax(const T* __restrict__ x, int64_t n, SpArgs a,
-                                                  float* scale_out) {
-  const Peers<NR> P = load_peers<NR>(a);
+__device__ __forceinline__ void phase_scale(const T* __restrict__ x, int64_t n, const SpArgs& a,
+                                            const Peers<NR>& P, float* scale_out) {
   uint32_t m = 0, bad = 0;
-  for (int64_t i = cta_lo(n) + threadIdx.x, e = cta_hi(n); i < e; i += kSpT) {
+  const int64_t ng = a.vec ? n / 16 : 0;
+  for (int64_t gi = cta_lo(ng) + threadIdx.x, e = cta_hi(ng); gi < e; gi += kSpT) {
+    float v[16];
+    In<T>::get16(x, gi * 16, v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t b = abs_bits(v[k]);
+      m = max(m, b);
+      bad |= b >= 0x7F800000u;
+    }
+  }
+  const int64_t t0 = ng * 16;
+  for (int64_t i = t0 + cta_lo(n - t0) + threadIdx.x, e = t0 + cta_hi(n - t0); i < e; i += kSpT) {
     const uint32_t b = abs_bits(In<T>::get(x, i));
     m = max(m, b);
     bad |= b >= 0x7F800000u;
@@ -123,35 +181,32 @@ __global__ void __launch_bounds__(kSpT) k_sp_amax(const T* __restrict__ x, int64
     if (m) atomicMax(a.scratch + kSpScrAmax, m);
     if (bad) atomicOr(a.scratch + kSpScrBad, 1u);
   }
-  if (!sp_last_cta(a.scratch + kSpScrTicketA)) return;
-  if (threadIdx.x != 0) return;
-  // s_r = fl(448 / A_r): 0 if non-finite, +inf if A_r = 0 or the ratio overflows (R14)
-  const uint32_t ab = a.scratch[kSpScrAmax];
-  float sr;
-  if (a.scratch[kSpScrBad]) {
-    sr = 0.0f;
-  } else if (ab == 0) {
-    sr = __int_as_float(0x7F800000);
-  } else {
-    sr = __fdiv_rn(448.0f, __uint_as_float(ab));
-  }
-  a.scratch[kSpScrAmax] = 0;
-  a.scratch[kSpScrBad] = 0;
+  grid_phase(a, kSpScrTicketA, kSpScrFlag1, false, [&] {
+    // s_r = fl(448 / A_r): 0 if non-finite, +inf if A_r = 0 or the ratio overflows (R14)
+    const uint32_t ab = a.scratch[kSpScrAmax];
+    float sr;
+    if (a.scratch[kSpScrBad]) sr = 0.0f;
+    else if (ab == 0) sr = __int_as_float(0x7F800000);
+    else sr = __fdiv_rn(448.0f, __uint_as_float(ab));
+    a.scratch[kSpScrAmax] = 0;
+    a.scratch[kSpScrBad] = 0;
 #pragma unroll
-  for (int q = 0; q < NR; ++q)
-    reinterpret_cast<volatile float*>(sp_flags(P.pad[q], kSpPadScales))[a.rank] = sr;
-  __threadfence_system();
-  release_all<NR>(P, kSpPadFlagScale, a.rank, a.epoch);
-  wait_epoch(sp_flags(a.pad, kSpPadFlagScale), NR, a.epoch);
-  const volatile float* sc = reinterpret_cast<const volatile float*>(sp_flags(a.pad, kSpPadScales));
-  float s = sc[0];
+    for (int q = 0; q < NR; ++q)
+      reinterpret_cast<volatile float*>(sp_flags(P.pad[q], kSpPadScales))[a.rank] = sr;
+    __threadfence_system();
+    release_all<NR>(P, kSpPadFlagScale, a.rank, a.epoch);
+    wait_epoch(sp_flags(a.pad, kSpPadFlagScale), NR, a.epoch);
+    // Eq. 4: the MIN of the ranks' scales; every rank zero / tiny -> 1
+    const volatile float* sc = reinterpret_cast<const volatile float*>(sp_flags(a.pad, kSpPadScales));
+    float s = sc[0];
 #pragma unroll
-  for (int q = 1; q < NR; ++q) s = fminf(s, sc[q]);
-  if (isinf(s)) s = 1.0f;                       // every rank zero / tiny
-  const float sinv = __fdiv_rn(1.0f, s);
-  a.scratch[kSpScrS] = __float_as_uint(s);
-  a.scratch[kSpScrSinv] = __float_as_uint(sinv);
-  if (scale_out) { scale_out[0] = s; scale_out[1] = sinv; }
+    for (int q = 1; q < NR; ++q) s = fminf(s, sc[q]);
+    if (isinf(s)) s = 1.0f;
+    const float sinv = __fdiv_rn(1.0f, s);
+    a.scratch[kSpScrS] = __float_as_uint(s);
+    a.scratch[kSpScrSinv] = __float_as_uint(sinv);
+    if (scale_out) { scale_out[0] = s; scale_out[1] = sinv; }
+  });
 }
 
 // 16 values -> 16 E4M3 codes of fl(x * s)
@@ -164,66 +219,60 @@ __device__ __forceinline__ uint4 quant16(const float* x, float s) {
   return c;
 }
 
-template <int NR>
-__device__ __forceinline__ void wait_done_prev(const SpArgs& a) {
+// ------------------------------------------------------------------ phase 2: quantize
+// PUSH: codes of x[0, n) to every rank's receive window at rank * n (all-gather);
+// else: to the own send window (reduce-scatter).  Waits first until every rank is done
+// with the previous epoch's windows; the last CTA then releases "data" to every rank.
+template <typename T, int NR, bool PUSH>
+__device__ __forceinline__ void phase_quant(const T* __restrict__ x, int64_t n, const SpArgs& a,
+                                            const Peers<NR>& P) {
   if (threadIdx.x == 0) wait_epoch(sp_flags(a.pad, kSpPadFlagDone), NR, a.epoch - 1);
   __syncthreads();
-}
-
-// ------------------------------------------------------------------ all-gather
-// PUSH = true: codes of x[0, m) go to every rank's receive window at rank * m (k_sp_push)
-// PUSH = false: codes of x[0, n) go to the own send window at 0 (k_sp_quant, RS)
-template <typename T, int NR, bool PUSH>
-__global__ void __launch_bounds__(kSpT) k_sp_quant(const T* __restrict__ x, int64_t n, SpArgs a) {
-  const Peers<NR> P = load_peers<NR>(a);
-  wait_done_prev<NR>(a);
-  const float s = __uint_as_float(a.scratch[kSpScrS]);
+  const float s = __uint_as_float(*(volatile uint32_t*)(a.scratch + kSpScrS));
   const int64_t dst_off = PUSH ? (int64_t)a.rank * n : 0;
-  const bool vec = a.vec;
-  if (vec) {
-    const int64_t ng = n / 16;
-    for (int64_t gi = cta_lo(ng) + threadIdx.x, e = cta_hi(ng); gi < e; gi += kSpT) {
-      float v[16];
-      In<T>::get16(x, gi * 16, v);
-      const uint4 c = quant16(v, s);
-      if (PUSH) {
+  uint8_t* own_send = P.send[0];
 #pragma unroll
-        for (int q = 0; q < NR; ++q) st128(P.recv[q] + dst_off + gi * 16, c);
-      } else {
-        st128(P.send[a.rank] + gi * 16, c);
-      }
+  for (int q = 1; q < NR; ++q) if (q == a.rank) own_send = P.send[q];
+  const int64_t ng = a.vec ? n / 16 : 0;
+  for (int64_t gi = cta_lo(ng) + threadIdx.x, e = cta_hi(ng); gi < e; gi += kSpT) {
+    float v[16];
+    In<T>::get16(x, gi * 16, v);
+    const uint4 c = quant16(v, s);
+    if (PUSH) {
+#pragma unroll
+      for (int q = 0; q < NR; ++q) st128(P.recv[q] + dst_off + gi * 16, c);
+    } else {
+      st128(own_send + gi * 16, c);
     }
   }
-  const int64_t tail0 = vec ? n / 16 * 16 : 0;
-  for (int64_t i = tail0 + cta_lo(n - tail0) + threadIdx.x, e = tail0 + cta_hi(n - tail0); i < e; i += kSpT) {
+  const int64_t t0 = ng * 16;
+  for (int64_t i = t0 + cta_lo(n - t0) + threadIdx.x, e = t0 + cta_hi(n - t0); i < e; i += kSpT) {
     const uint8_t c = (uint8_t)(e4m3x2(__fmul_rn(In<T>::get(x, i), s), 0.0f) & 0xFFu);
     if (PUSH) {
 #pragma unroll
       for (int q = 0; q < NR; ++q) P.recv[q][dst_off + i] = c;
     } else {
-      P.send[a.rank][i] = c;
+      own_send[i] = c;
     }
   }
-  if (sp_last_cta(a.scratch + kSpScrTicketB) && threadIdx.x == 0)
-    release_all<NR>(P, kSpPadFlagData, a.rank, a.epoch);
-}
-
-template <typename O> struct Out;
-template <> struct Out<float> {
-  static __device__ __forceinline__ void put(float* p, int64_t i, float v) { p[i] = v; }
-};
-template <> struct Out<__nv_bfloat16> {
-  static __device__ __forceinline__ void put(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
-};
-
-// wait for every rank's codes, copy them out and / or dequantize fl(dec(c) * sinv)
-template <typename O, int NR>
-__global__ void __launch_bounds__(kSpT) k_sp_gather(int64_t total, uint8_t* codes_out, O* out, SpArgs a) {
-  const Peers<NR> P = load_peers<NR>(a);
+  grid_phase(a, kSpScrTicketB, kSpScrFlag2, true, [&] { release_all<NR>(P, kSpPadFlagData, a.rank, a.epoch); });
   if (threadIdx.x == 0) wait_epoch(sp_flags(a.pad, kSpPadFlagData), NR, a.epoch);
   __syncthreads();
-  const float sinv = __uint_as_float(a.scratch[kSpScrSinv]);
-  const uint8_t* src = P.recv[a.rank];
+}
+
+// ------------------------------------------------------------------ all-gather kernel
+template <typename T, typename O, int NR>
+__global__ void __launch_bounds__(kSpT) k_sp_allgather(const T* __restrict__ x, int64_t m, uint8_t* codes_out,
+                                                       O* out, float* scale_out, SpArgs a) {
+  const Peers<NR> P = load_peers<NR>(a);
+  phase_scale<T, NR>(x, m, a, P, scale_out);
+  phase_quant<T, NR, true>(x, m, a, P);
+  // phase 3: every rank's codes have landed: copy them out and / or dequantize
+  const float sinv = __uint_as_float(*(volatile uint32_t*)(a.scratch + kSpScrSinv));
+  const int64_t total = m * NR;
+  const uint8_t* src = P.recv[0];
+#pragma unroll
+  for (int q = 1; q < NR; ++q) if (q == a.rank) src = P.recv[q];
   if (codes_out || out) {
     const int64_t ng = a.vec ? total / 16 : 0;
     for (int64_t gi = cta_lo(ng) + threadIdx.x, e = cta_hi(ng); gi < e; gi += kSpT) {
@@ -233,7 +282,8 @@ __global__ void __launch_bounds__(kSpT) k_sp_gather(int64_t total, uint8_t* code
         float d[16];
         dec_e4m3x4(c.x, d); dec_e4m3x4(c.y, d + 4); dec_e4m3x4(c.z, d + 8); dec_e4m3x4(c.w, d + 12);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) Out<O>::put(out, gi * 16 + k, __fmul_rn(d[k], sinv));
+        for (int k = 0; k < 16; ++k) d[k] = __fmul_rn(d[k], sinv);
+        Out<O>::put16(out, gi * 16, d);
       }
     }
     const int64_t t0 = ng * 16;
@@ -247,19 +297,22 @@ __global__ void __launch_bounds__(kSpT) k_sp_gather(int64_t total, uint8_t* code
       }
     }
   }
-  if (sp_last_cta(a.scratch + kSpScrTicketC) && threadIdx.x == 0)
+  if (sp_last_cta(a.scratch + kSpScrTicketC, false) && threadIdx.x == 0) {
+    __threadfence_system();
     release_all<NR>(P, kSpPadFlagDone, a.rank, a.epoch);
+  }
 }
 
-// ------------------------------------------------------------------ reduce-scatter
-// wait for every rank's quantized gradient, pull chunk `rank` (m codes) from each send
-// window over NVLink, sum in rank order (binary32, R12), out = fl(S * fl(1/s)) (R32)
-template <typename O, int NR>
-__global__ void __launch_bounds__(kSpT) k_sp_pull(int64_t m, O* out, SpArgs a) {
+// ------------------------------------------------------------------ reduce-scatter kernel
+// phase 3: pull chunk `rank` (m codes) from every rank's send window over NVLink, sum in
+// rank order (binary32, R12), out = fl(S * fl(1/s)) (R32)
+template <typename T, typename O, int NR>
+__global__ void __launch_bounds__(kSpT) k_sp_reduce_scatter(const T* __restrict__ dy, int64_t m, O* out,
+                                                            float* scale_out, SpArgs a) {
   const Peers<NR> P = load_peers<NR>(a);
-  if (threadIdx.x == 0) wait_epoch(sp_flags(a.pad, kSpPadFlagData), NR, a.epoch);
-  __syncthreads();
-  const float sinv = __uint_as_float(a.scratch[kSpScrSinv]);
+  phase_scale<T, NR>(dy, m * NR, a, P, scale_out);
+  phase_quant<T, NR, false>(dy, m * NR, a, P);
+  const float sinv = __uint_as_float(*(volatile uint32_t*)(a.scratch + kSpScrSinv));
   const int64_t base = (int64_t)a.rank * m;
   const int64_t ng = a.vec ? m / 16 : 0;
   for (int64_t gi = cta_lo(ng) + threadIdx.x, e = cta_hi(ng); gi < e; gi += kSpT) {
@@ -276,7 +329,8 @@ __global__ void __launch_bounds__(kSpT) k_sp_pull(int64_t m, O* out, SpArgs a) {
       for (int k = 0; k < 16; ++k) S[k] = __fadd_rn(S[k], d[k]);
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) Out<O>::put(out, gi * 16 + k, __fmul_rn(S[k], sinv));
+    for (int k = 0; k < 16; ++k) S[k] = __fmul_rn(S[k], sinv);
+    Out<O>::put16(out, gi * 16, S);
   }
   const int64_t t0 = ng * 16;
   for (int64_t i = t0 + cta_lo(m - t0) + threadIdx.x, e = t0 + cta_hi(m - t0); i < e; i += kSpT) {
@@ -289,12 +343,15 @@ __global__ void __launch_bounds__(kSpT) k_sp_pull(int64_t m, O* out, SpArgs a) {
     }
     Out<O>::put(out, i, __fmul_rn(S, sinv));
   }
-  if (sp_last_cta(a.scratch + kSpScrTicketC) && threadIdx.x == 0)
+  if (sp_last_cta(a.scratch + kSpScrTicketC, false) && threadIdx.x == 0) {
+    __threadfence_system();
     release_all<NR>(P, kSpPadFlagDone, a.rank, a.epoch);
+  }
 }
 
-template <typename K>
-int sp_grid(K kernel, int64_t work) {
+// cooperative launch: the phases' grid barriers need every CTA resident
+template <typename K, typename... Args>
+cudaError_t coop_launch(K kernel, int64_t work, cudaStream_t s, Args... args) {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -303,83 +360,59 @@ int sp_grid(K kernel, int64_t work) {
   }
   int per = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kSpT, 0);
+  // 2 CTAs per SM: the three grid barriers and their flag polling cost more than the
+  // extra occupancy buys (measured 1, 2, 4, 8 per SM; FP8LM_SP_CTAS_PER_SM overrides)
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("FP8LM_SP_CTAS_PER_SM");
+    cap = e ? atoi(e) : 2;
+  }
+  if (cap > 0 && cap < per) per = cap;
   const int64_t want = (work + kSpT - 1) / kSpT;
   int64_t grid = (int64_t)sms * (per > 0 ? per : 1);
   if (want < grid) grid = want;
-  return (int)(grid < 1 ? 1 : grid);
+  if (grid < 1) grid = 1;
+  void* params[] = {&args...};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3((unsigned)grid), dim3(kSpT),
+                                     params, 0, s);
 }
 
-template <typename T, int NR>
-cudaError_t sp_amax(const void* x, int64_t n, const SpArgs& a, float* scale_out, cudaStream_t s) {
-  auto k = k_sp_amax<T, NR>;
-  k<<<sp_grid(k, n), kSpT, 0, s>>>(static_cast<const T*>(x), n, a, scale_out);
-  return cudaGetLastError();
+template <int NR, typename T>
+cudaError_t sp_allgather_t(const void* x, int64_t m, uint8_t* codes_out, void* out, int out_dtype,
+                           float* scale_out, const SpArgs& a, cudaStream_t s) {
+  ProfScope ps_(P_SP_ALLGATHER, s);
+  const int64_t work = std::max<int64_t>(m, m * NR / 16);
+  if (out_dtype == FP8LM_BF16)
+    return coop_launch(k_sp_allgather<T, __nv_bfloat16, NR>, work, s, static_cast<const T*>(x), m, codes_out,
+                       static_cast<__nv_bfloat16*>(out), scale_out, a);
+  return coop_launch(k_sp_allgather<T, float, NR>, work, s, static_cast<const T*>(x), m, codes_out,
+                     static_cast<float*>(out), scale_out, a);
 }
 
 template <int NR>
 cudaError_t sp_allgather_n(const void* x, int x_dtype, int64_t m, uint8_t* codes_out, void* out,
                            int out_dtype, float* scale_out, const SpArgs& a, cudaStream_t s) {
-  cudaError_t e;
-  {
-    ProfScope ps_(P_SP_AMAX, s);
-    e = x_dtype == FP8LM_F32 ? sp_amax<float, NR>(x, m, a, scale_out, s)
-                             : sp_amax<__nv_bfloat16, NR>(x, m, a, scale_out, s);
-    if (e != cudaSuccess) return e;
-  }
-  {
-    ProfScope ps_(P_SP_PUSH, s);
-    if (x_dtype == FP8LM_F32) {
-      auto k = k_sp_quant<float, NR, true>;
-      k<<<sp_grid(k, m / 16 + 1), kSpT, 0, s>>>(static_cast<const float*>(x), m, a);
-    } else {
-      auto k = k_sp_quant<__nv_bfloat16, NR, true>;
-      k<<<sp_grid(k, m / 16 + 1), kSpT, 0, s>>>(static_cast<const __nv_bfloat16*>(x), m, a);
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  ProfScope ps_(P_SP_GATHER, s);
-  const int64_t total = m * NR;
-  if (out_dtype == FP8LM_BF16) {
-    auto k = k_sp_gather<__nv_bfloat16, NR>;
-    k<<<sp_grid(k, total / 16 + 1), kSpT, 0, s>>>(total, codes_out, static_cast<__nv_bfloat16*>(out), a);
-  } else {
-    auto k = k_sp_gather<float, NR>;
-    k<<<sp_grid(k, total / 16 + 1), kSpT, 0, s>>>(total, codes_out, static_cast<float*>(out), a);
-  }
-  return cudaGetLastError();
+  return x_dtype == FP8LM_F32 ? sp_allgather_t<NR, float>(x, m, codes_out, out, out_dtype, scale_out, a, s)
+                              : sp_allgather_t<NR, __nv_bfloat16>(x, m, codes_out, out, out_dtype, scale_out, a, s);
+}
+
+template <int NR, typename T>
+cudaError_t sp_reduce_scatter_t(const void* dy, int64_t m, void* out, int out_dtype, float* scale_out,
+                                const SpArgs& a, cudaStream_t s) {
+  ProfScope ps_(P_SP_REDUCE_SCATTER, s);
+  const int64_t work = m * NR;
+  if (out_dtype == FP8LM_BF16)
+    return coop_launch(k_sp_reduce_scatter<T, __nv_bfloat16, NR>, work, s, static_cast<const T*>(dy), m,
+                       static_cast<__nv_bfloat16*>(out), scale_out, a);
+  return coop_launch(k_sp_reduce_scatter<T, float, NR>, work, s, static_cast<const T*>(dy), m,
+                     static_cast<float*>(out), scale_out, a);
 }
 
 template <int NR>
 cudaError_t sp_reduce_scatter_n(const void* dy, int dtype, int64_t m, void* out, int out_dtype,
                                 float* scale_out, const SpArgs& a, cudaStream_t s) {
-  const int64_t n = m * NR;
-  cudaError_t e;
-  {
-    ProfScope ps_(P_SP_AMAX, s);
-    e = dtype == FP8LM_F32 ? sp_amax<float, NR>(dy, n, a, scale_out, s)
-                           : sp_amax<__nv_bfloat16, NR>(dy, n, a, scale_out, s);
-    if (e != cudaSuccess) return e;
-  }
-  {
-    ProfScope ps_(P_SP_QUANT, s);
-    if (dtype == FP8LM_F32) {
-      auto k = k_sp_quant<float, NR, false>;
-      k<<<sp_grid(k, n / 16 + 1), kSpT, 0, s>>>(static_cast<const float*>(dy), n, a);
-    } else {
-      auto k = k_sp_quant<__nv_bfloat16, NR, false>;
-      k<<<sp_grid(k, n / 16 + 1), kSpT, 0, s>>>(static_cast<const __nv_bfloat16*>(dy), n, a);
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  ProfScope ps_(P_SP_PULL, s);
-  if (out_dtype == FP8LM_BF16) {
-    auto k = k_sp_pull<__nv_bfloat16, NR>;
-    k<<<sp_grid(k, m / 16 + 1), kSpT, 0, s>>>(m, static_cast<__nv_bfloat16*>(out), a);
-  } else {
-    auto k = k_sp_pull<float, NR>;
-    k<<<sp_grid(k, m / 16 + 1), kSpT, 0, s>>>(m, static_cast<float*>(out), a);
-  }
-  return cudaGetLastError();
+  return dtype == FP8LM_F32 ? sp_reduce_scatter_t<NR, float>(dy, m, out, out_dtype, scale_out, a, s)
+                            : sp_reduce_scatter_t<NR, __nv_bfloat16>(dy, m, out, out_dtype, scale_out, a, s);
 }
 
 }  // namespace
