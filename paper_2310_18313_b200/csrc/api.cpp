@@ -240,7 +240,7 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
   p->off_acc_state = take(sizeof(uint32_t) * std::max(3 * T, 1));
   p->off_sat_part = take(sizeof(uint32_t) * std::max(T, 1));
   p->off_sat_acc = take(sizeof(uint32_t) * std::max(T, 1));
-  p->off_ctr = take(sizeof(uint32_t) * 4);
+  p->off_ctr = take(sizeof(uint32_t) * kCtrWords);
   p->off_acc_end = off;
   if (mode == FP8LM_MODE_NCCL) {
     p->off_send = take((size_t)(p->shard * nranks));

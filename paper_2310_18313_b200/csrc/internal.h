@@ -38,7 +38,7 @@ struct DevPlan {
   uint8_t* recv;            // [N*S]     NCCL all-to-all receive buffer
   uint8_t* sim_codes;       // [nsim*total] simulated ranks' quantized codes
   uint32_t* sat_acc;        // [T]       saturation counts of the step (zero at rest)
-  uint32_t* counters;       // [4]       grid_last_block tickets (zero at rest)
+  uint32_t* counters;       // [8]       grid_last_block tickets, grid barrier (zero at rest)
   // mode ZERO: owned tensors j = 0..T_own-1 (ascending t)
   int32_t T_own;
   const int64_t* own_gpos;  // [T_own] full-layout offset of owned tensor j
@@ -46,7 +46,7 @@ struct DevPlan {
   float* gsinv_own;         // [T_own] compact copy of g_scale_inv (written by the reduce tail)
 };
 
-constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2;
+constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2, kCtrFix = 3, kCtrFixGen = 4, kCtrWords = 8;
 
 // ---------------------------------------------------------------- mode P2P windows
 // Signal / exchange pad of one rank (bytes): three flag arrays (one u32 epoch slot per
