@@ -330,11 +330,19 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # clock sampler runs through a ~1 s untimed soak and the timed region
+    # clock sampler runs through a ~1 s untimed soak and the timed region.  Every rank
+    # must run the SAME number of soak steps (each step is a collective), so the count is
+    # derived from the warm-up's pace and agreed on (max over ranks) before the soak.
     sampler = None if args.quick else ClockSampler(local)
-    t_soak = time.perf_counter()
-    while sampler is not None and time.perf_counter() - t_soak < 1.0:
-        step()
+    if sampler is not None:
+        t0 = time.perf_counter()
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        per = max((time.perf_counter() - t0) / 3, 1e-5)
+        n_soak = int(max_over_ranks(float(min(20000, max(1, int(1.0 / per)))), world))
+        for _ in range(n_soak):
+            step()
         torch.cuda.synchronize()
 
     # ---------------- timed region: K steps, CUDA events on the launch stream.  A clean
