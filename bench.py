@@ -414,6 +414,16 @@ def main():
                     "frac": achieved / hbm, "peak_kind": hbm_kind, "traffic": None,
                     "alg_bytes_per_launch": bpp * np_, "avg_launch_ms": per_launch_ms,
                     "share_of_step": ours[dom]["ms"] / (ms_prof_local * args.steps)}
+    if roof is not None:
+        # DRAM bytes per launch of the same kernel on the same workload, from the committed
+        # `ncu --set full` capture (tools/ncu_traffic.py); null when none was taken
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")))
+            ent = tr[args.config + ("" if N == 1 else f"/n{N}/{args.exchange}")][dom]
+            roof["traffic"] = ent["dram_bytes_per_launch"]
+            roof["traffic_source"] = "profiles/r1/ncu_traffic.json (" + ent["source"] + ")"
+        except (OSError, KeyError, ValueError):
+            pass
     launches = int(sum(v["launches"] for v in ours.values()) / args.steps)
     breakdown = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
                  for k, v in prof.items()}
