@@ -54,6 +54,8 @@ def assert_state_equal(dev, ref: OA.OptState, where=""):
         assert (s, si, a) == (r.scale, r.scale_inv, r.amax), (where, name, (s, si, a), (r.scale, r.scale_inv, r.amax))
 
 
-def oracle_init(plan, w0_flat):
-    w0 = to_np_f32(w0_flat)
-    return [OA.init_state(w0[plan.offsets[t]: plan.offsets[t] + plan.numels[t]]) for t in range(plan.T)]
+def oracle_init(plan, w0_flat, sub=None):
+    """Oracle initial states of the tensors in `sub` (default: all), copying only their
+    slices of the device buffer to the host."""
+    sub = range(plan.T) if sub is None else sub
+    return [OA.init_state(to_np_f32(w0_flat[plan.offsets[t]: plan.offsets[t] + plan.numels[t]])) for t in sub]
