@@ -859,8 +859,8 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
   if (rc) return rc;
   const bool delayed = w_hist != nullptr;
   if (delayed && (hist_slot < 0 || hist_slot >= 16)) return fail(FP8LM_EINVAL, "dp_step: hist_slot not in [0, 16)");
-  if ((p->mode != FP8LM_MODE_LOCAL && p->mode != FP8LM_MODE_P2P) || p->T == 0 ||
-      (delayed && p->mode != FP8LM_MODE_LOCAL)) {
+  if ((p->mode != FP8LM_MODE_LOCAL && p->mode != FP8LM_MODE_P2P && p->mode != FP8LM_MODE_ZERO) ||
+      p->T == 0 || (delayed && p->mode != FP8LM_MODE_LOCAL)) {
     rc = fp8lm_grad_allreduce(p, comm, grads, src_dtype, s_g, skip, g8, g_scale, g_scale_inv, sat,
                               mu, stream);
     if (rc) return rc;
@@ -868,6 +868,26 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
       return fp8lm_adam_step_delayed(p, g8, g_scale_inv, m1, v, master, w8, hp, skip, w_hist,
                                      hist_slot, stream);
     return fp8lm_adam_step(p, g8, g_scale_inv, m1, v, master, w8, hp, skip, stream);
+  }
+  if (p->mode == FP8LM_MODE_ZERO) {
+    // the owner reduce runs Adam pass 1 on the reduced codes of its whole tensors
+    if (!p->p2p_ready) return fail(FP8LM_EINVAL, "dp_step: mode ZERO needs fp8lm_peer_setup first");
+    if (!hp || !g_scale || !g_scale_inv || !sat || !m1 || !v || !master || !w8)
+      return fail(FP8LM_EINVAL, "dp_step: NULL argument");
+    if (p->own->T > 0 && (!g8 || !aligned(g8, 256))) return fail(FP8LM_EINVAL, "dp_step: g8 NULL or misaligned");
+    const void* srcs[1];
+    int nsrc = 0;
+    if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
+    const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
+    uint8_t* dst[1] = {p->win_send};
+    CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
+    CUDA_TRY(launch_reduce_owner_a1(p->dev, p->own->dev, p2p_args(p, p->epoch), s_g, tail, g8, *m1, *v,
+                                    *master, *w8, *hp, skip, S(stream)));
+    CUDA_TRY(launch_adam(p->own->dev, g8, p->dev.gsinv_own, *m1, *v, *master, *w8, *hp, skip, S(stream),
+                         /*pass1=*/false));
+    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p, ++p->epoch_w8),
+                             static_cast<const uint8_t*>(w8->data), *w8, S(stream)));
+    return FP8LM_OK;
   }
   if (p->mode == FP8LM_MODE_P2P) {
     // the exchange kernel runs Adam pass 1 on its own shard; maxima combined in its tail

@@ -223,6 +223,11 @@ cudaError_t launch_sp_allgather(const void* x, int x_dtype, int64_t m, uint8_t* 
                                 int out_dtype, float* scale_out, const SpArgs& a, cudaStream_t s);
 cudaError_t launch_sp_reduce_scatter(const void* dy, int dtype, int64_t m, void* out, int out_dtype,
                                      float* scale_out, const SpArgs& a, cudaStream_t s);
+cudaError_t launch_reduce_owner_a1(const DevPlan& p, const DevPlan& o, const P2PArgs& x, const float* s_g,
+                                   const TailArgs& tail, uint8_t* g8, const fp8lm_stensors& m1,
+                                   const fp8lm_stensors& v, const fp8lm_stensors& w,
+                                   const fp8lm_stensors& w8, const fp8lm_adam_hp& hp,
+                                   const int32_t* skip, cudaStream_t s);
 cudaError_t launch_dq_single(const void* codes, int fmt, int64_t n, const float* scale_inv,
                              float* dst, cudaStream_t s);
 int num_sms();

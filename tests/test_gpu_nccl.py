@@ -5,7 +5,8 @@ oracle, for both exchange modes:
   p2p:  the same arithmetic with the MIN exchanged through peer pads and reduce-scatter
         + reduce + all-gather fused in one kernel over NVLink peer memory;
   zero: FP8 ZeRO (Alg. 1): the owner of each whole tensor reduces it from every rank's
-        send window and runs AdamW on it alone; w8 + scalars replicated by peer stores.
+        send window and runs AdamW on it alone (through fp8lm_dp_step: pass 1 inside the
+        owner reduce; "unfused": the three calls); w8 + scalars replicated by peer stores.
 Needs >= 2 GPUs (gpurun --gpus 2 / 4)."""
 import os
 import socket
@@ -39,7 +40,8 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("mode", ["nccl", "p2p", "p2p_unfused", "zero", "p2p_delayed", "zero_delayed"])
+@pytest.mark.parametrize("mode", ["nccl", "p2p", "p2p_unfused", "zero", "zero_unfused", "p2p_delayed",
+                                  "zero_delayed"])
 @pytest.mark.parametrize("n", [2, 4])
 def test_multi_gpu_bit_exact(n, mode):
     if _ngpus() < n:
@@ -49,6 +51,10 @@ def test_multi_gpu_bit_exact(n, mode):
            os.path.join(ROOT, "tests", "dist_worker.py"), "--steps", "3",
            "--mode", mode.split("_")[0]] + (["--unfused"] if "unfused" in mode else []) + \
           (["--delayed"] if "delayed" in mode else [])
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    for _ in range(3):          # a freshly probed port can be taken before torchrun binds it
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            break
+        cmd[cmd.index("--master-port") + 1] = str(_port())
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"{mode.upper()} parity N={n}: OK" in r.stdout

@@ -75,6 +75,10 @@ def test_multi_gpu_converter(n):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "sp_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    for _ in range(3):          # a freshly probed port can be taken before torchrun binds it
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            break
+        cmd[cmd.index("--master-port") + 1] = str(_port())
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"SP parity N={n}: OK" in r.stdout
