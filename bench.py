@@ -389,11 +389,13 @@ def main():
     roof = None
     kparams = sum(dp.layout.numels) if zero else params     # AdamW runs on owned tensors only
     if dom == "reduce_p2p":
-        # fused reduce-scatter + all-gather over NVLink peer memory: every direction of
-        # every link carries 2(N-1)/N bytes per parameter (read responses + peer stores);
-        # the ZeRO owner reduce only pulls (N-1)/N (the w8 broadcast is a separate kernel)
+        # reduce-scatter over NVLink peer memory: every link direction carries (N-1)/N
+        # bytes per parameter of read responses.  The fused JIT step (fp8lm_dp_step) pulls
+        # the all-gather inside pass 2, so its exchange kernel moves only those; the
+        # unfused path (delayed state scaling) also stores the all-gather from the
+        # exchange kernel: 2(N-1)/N.  The ZeRO owner reduce only pulls (N-1)/N.
         per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
-        nvb = (1.0 if zero else 2.0) * (N - 1) / N * params
+        nvb = (2.0 if (delayed and not zero) else 1.0) * (N - 1) / N * params
         achieved = nvb / (per_launch_ms / 1e3) / 1e9
         roof = {"bound": "nvlink", "kernel": dom, "achieved": achieved, "peak": NVLINK_PEER_GBS,
                 "unit": "GB/s", "frac": achieved / NVLINK_PEER_GBS,
@@ -427,6 +429,13 @@ def main():
     launches = int(sum(v["launches"] for v in ours.values()) / args.steps)
     breakdown = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
                  for k, v in prof.items()}
+    if world > 1:
+        # the same kernel on every rank: a spread here is cross-rank skew (a rank waiting in
+        # the next step's scale exchange for a slower one), not kernel work
+        for k in sorted(breakdown):
+            v = breakdown[k]["ms_per_step"]
+            breakdown[k]["ms_per_step_min_over_ranks"] = -max_over_ranks(-v, world)
+            breakdown[k]["ms_per_step_max_over_ranks"] = max_over_ranks(v, world)
 
     # ---------------- e2e: host gradients (pinned) -> device, step, results -> host
     e2e = None

@@ -903,10 +903,20 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
     uint8_t* dst[1] = {p->win_send};
     CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
-    CUDA_TRY(launch_reduce_p2p_a1(p->dev, p2p_args(p, p->epoch), s_g, tail, g8, *m1, *v, *master, *w8,
-                                  *hp, skip, S(stream)));
+    // the exchange leaves each rank's reduced shard in its own window; pass 2 pulls the
+    // other shards' codes from the peers' windows (the all-gather, overlapped with pass 2)
+    const P2PArgs x = p2p_args(p, p->epoch);
+    CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip,
+                                  S(stream)));
+    // pass 2 starts its work order at this rank's shard: the ranks pull from different
+    // owners at any moment instead of all from one (FP8LM_PULL_ROT=0 disables, diagnosis)
+    static const bool rotate = !getenv("FP8LM_PULL_ROT") || atoi(getenv("FP8LM_PULL_ROT")) != 0;
+    const int64_t lo = p->shard * p->rank;
+    const auto first = std::lower_bound(p->items.begin(), p->items.end(), lo,
+                                        [](const ShardItem& a, int64_t v) { return a.pos < v; });
+    const int64_t rot = rotate ? (int64_t)(first - p->items.begin()) : 0;
     CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream),
-                         /*pass1=*/false));
+                         /*pass1=*/false, x.tab, p->shard, rot));
     return FP8LM_OK;
   }
   // LOCAL: the codes quantize produces are final, so Adam pass 1 runs in the same kernel

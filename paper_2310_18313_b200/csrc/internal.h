@@ -191,7 +191,8 @@ cudaError_t launch_adam(const DevPlan& p, const uint8_t* g8, const float* g_sinv
                         const fp8lm_stensors& m1, const fp8lm_stensors& v,
                         const fp8lm_stensors& w, const fp8lm_stensors& w8,
                         const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s,
-                        bool pass1 = true);
+                        bool pass1 = true, const PeerTable* pull_tab = nullptr,
+                        int64_t pull_shard = 0, int64_t rot = 0);
 cudaError_t launch_adam_fused_local(const DevPlan& p, const void* grads, int src_dtype,
                                    const float* s_g, uint8_t* g8, const TailArgs& tail,
                                    const fp8lm_stensors& m1, const fp8lm_stensors& v,

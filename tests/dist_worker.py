@@ -110,7 +110,13 @@ def main():
         for t in range(plan.T):
             p = res["per_tensor"][t]
             sl = slice(plan.offsets[t], plan.offsets[t] + plan.numels[t])
-            if g8 is not None:
+            if g8 is not None and args.mode == "p2p" and not args.unfused and not args.delayed:
+                # fused P2P step: the all-gather is pulled inside pass 2, so this rank's
+                # window holds its own shard's codes only (include/fp8lm.h, fp8lm_dp_step)
+                lo, hi = plan.shard_begin(rank), plan.shard_begin(rank) + plan.shard_bytes
+                a, b = max(lo, sl.start), min(hi, sl.stop)
+                codes_ok = a >= b or np.array_equal(g8[a:b], p["codes"][a - sl.start:b - sl.start])
+            elif g8 is not None:
                 codes_ok = np.array_equal(g8[sl], p["codes"])
             elif plan.owner(t) == rank:                       # ZeRO: only the owner reduces t
                 j = [tt for tt, _ in dp.layout.entries].index(t)

@@ -22,6 +22,7 @@ import torch.distributed as dist  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="gpt-125m")
+    ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--iters", type=int, default=20)
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
@@ -30,7 +31,7 @@ def main():
     rank, N = dist.get_rank(), dist.get_world_size()
     import paper_2310_18313_b200 as B
     import synth
-    specs = synth.gpt_gradient_set(args.config, None)
+    specs = synth.gpt_gradient_set(args.config, args.layers)
     numels = [s.numel for s in specs]
     comm = B.Comm.from_torch_distributed()
     pp = B.Plan(numels, mode=B.MODE_P2P, nranks=N, rank=rank)
@@ -114,7 +115,8 @@ def main():
     b = timeit(only_a)
     c = timeit(both)
     if rank == 0:
-        print(json.dumps({"config": args.config, "N": N, "T": T, "exchange_ms": a, "adam_ms": b,
+        print(json.dumps({"config": args.config, "layers": args.layers,
+                          "p2p_per_sm": os.environ.get("FP8LM_P2P_PER_SM"), "N": N, "T": T, "exchange_ms": a, "adam_ms": b,
                           "both_ms": c, "sum_ms": a + b, "max_ms": max(a, b)}), flush=True)
     comm.close()
     dist.destroy_process_group()
