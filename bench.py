@@ -388,7 +388,22 @@ def main():
     dom = max(ours, key=lambda k: ours[k]["ms"]) if ours else None
     roof = None
     kparams = sum(dp.layout.numels) if zero else params     # AdamW runs on owned tensors only
-    if dom == "reduce_p2p":
+    if zero and dom == "adam_pass2" and N > 1:
+        # ZeRO dp_step: the owner's pass 2 also stores every w8 code into the N-1 peers'
+        # windows, (N-1) bytes per owned parameter out of this GPU over NVLink, under its
+        # own 12 B/param of HBM traffic; the link is the bound (the HBM fraction rides along)
+        per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
+        nvb = (N - 1) * kparams
+        achieved = nvb / (per_launch_ms / 1e3) / 1e9
+        hbm_ach = KERNEL_BYTES["adam_pass2"] * kparams / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "nvlink", "kernel": dom, "achieved": achieved, "peak": NVLINK_PEER_GBS,
+                "unit": "GB/s", "frac": achieved / NVLINK_PEER_GBS,
+                "peak_kind": "measured peer copy per direction (B200_PROFILING.md); 900 nominal",
+                "frac_of_nominal_900": achieved / 900.0, "traffic": None,
+                "hbm_achieved": hbm_ach, "hbm_frac": hbm_ach / hbm,
+                "alg_bytes_per_launch": nvb, "avg_launch_ms": per_launch_ms,
+                "share_of_step": ours[dom]["ms"] / (ms_prof_local * args.steps)}
+    elif dom == "reduce_p2p":
         # reduce-scatter over NVLink peer memory: every link direction carries (N-1)/N
         # bytes per parameter of read responses.  The fused JIT step (fp8lm_dp_step) pulls
         # the all-gather inside pass 2, so its exchange kernel moves only those; the

@@ -883,10 +883,20 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
     CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
     CUDA_TRY(launch_reduce_owner_a1(p->dev, p->own->dev, p2p_args(p, p->epoch), s_g, tail, g8, *m1, *v,
                                     *master, *w8, *hp, skip, S(stream)));
-    CUDA_TRY(launch_adam(p->own->dev, g8, p->dev.gsinv_own, *m1, *v, *master, *w8, *hp, skip, S(stream),
-                         /*pass1=*/false));
-    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p, ++p->epoch_w8),
-                             static_cast<const uint8_t*>(w8->data), *w8, S(stream)));
+    // pass 2 on the owned tensors also stores every w8 group into every rank's window
+    // (the broadcast overlaps the HBM-bound pass); its last CTA publishes the scalars
+    Pass2Ext ext;
+    ext.bcast = p2p_args(p, ++p->epoch_w8);
+    ext.own_gpos = p->dev.own_gpos;
+    ext.own2full = p->dev.own2full;
+    ext.T_full = p->T;
+    if (p->own->dev.n_items > 0) {
+      CUDA_TRY(launch_adam(p->own->dev, g8, p->dev.gsinv_own, *m1, *v, *master, *w8, *hp, skip,
+                           S(stream), /*pass1=*/false, &ext));
+    } else {   // a rank that owns nothing still meets the others at flag W8
+      CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, ext.bcast, static_cast<const uint8_t*>(w8->data),
+                               *w8, S(stream)));
+    }
     return FP8LM_OK;
   }
   if (p->mode == FP8LM_MODE_P2P) {
@@ -914,9 +924,12 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
     const int64_t lo = p->shard * p->rank;
     const auto first = std::lower_bound(p->items.begin(), p->items.end(), lo,
                                         [](const ShardItem& a, int64_t v) { return a.pos < v; });
-    const int64_t rot = rotate ? (int64_t)(first - p->items.begin()) : 0;
+    Pass2Ext ext;
+    ext.pull_tab = x.tab;
+    ext.pull_shard = p->shard;
+    ext.rot = rotate ? (int64_t)(first - p->items.begin()) : 0;
     CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream),
-                         /*pass1=*/false, x.tab, p->shard, rot));
+                         /*pass1=*/false, &ext));
     return FP8LM_OK;
   }
   // LOCAL: the codes quantize produces are final, so Adam pass 1 runs in the same kernel

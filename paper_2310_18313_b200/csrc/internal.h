@@ -99,6 +99,19 @@ struct SpArgs {
   bool vec;            // 16-element vector paths (sizes multiples of 16, aligned buffers)
 };
 
+// pass 2 of the fused multi-GPU steps (fp8lm_dp_step)
+struct Pass2Ext {
+  // mode P2P: the all-gather pulled from the owners' g8 windows, work order rotated
+  const PeerTable* pull_tab = nullptr;
+  int64_t pull_shard = 0;
+  int64_t rot = 0;
+  // mode ZERO: w8 stored into every rank's window (tab == nullptr: off)
+  P2PArgs bcast{};
+  const int64_t* own_gpos = nullptr;
+  const int32_t* own2full = nullptr;
+  int T_full = 0;
+};
+
 // outputs of the Eq. 6 / mu tail of fp8lm_grad_allreduce
 struct TailArgs {
   int nranks;
@@ -191,8 +204,7 @@ cudaError_t launch_adam(const DevPlan& p, const uint8_t* g8, const float* g_sinv
                         const fp8lm_stensors& m1, const fp8lm_stensors& v,
                         const fp8lm_stensors& w, const fp8lm_stensors& w8,
                         const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s,
-                        bool pass1 = true, const PeerTable* pull_tab = nullptr,
-                        int64_t pull_shard = 0, int64_t rot = 0);
+                        bool pass1 = true, const Pass2Ext* ext = nullptr);
 cudaError_t launch_adam_fused_local(const DevPlan& p, const void* grads, int src_dtype,
                                    const float* s_g, uint8_t* g8, const TailArgs& tail,
                                    const fp8lm_stensors& m1, const fp8lm_stensors& v,
