@@ -405,12 +405,11 @@ def main():
                 "share_of_step": ours[dom]["ms"] / (ms_prof_local * args.steps)}
     elif dom == "reduce_p2p":
         # reduce-scatter over NVLink peer memory: every link direction carries (N-1)/N
-        # bytes per parameter of read responses.  The fused JIT step (fp8lm_dp_step) pulls
-        # the all-gather inside pass 2, so its exchange kernel moves only those; the
-        # unfused path (delayed state scaling) also stores the all-gather from the
-        # exchange kernel: 2(N-1)/N.  The ZeRO owner reduce only pulls (N-1)/N.
+        # bytes per parameter of read responses.  fp8lm_dp_step pulls the all-gather
+        # inside the AdamW pass that encodes the states, so the exchange kernel moves
+        # only those; the ZeRO owner reduce pulls (N-1)/N as well.
         per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
-        nvb = (2.0 if (delayed and not zero) else 1.0) * (N - 1) / N * params
+        nvb = 1.0 * (N - 1) / N * params
         achieved = nvb / (per_launch_ms / 1e3) / 1e9
         roof = {"bound": "nvlink", "kernel": dom, "achieved": achieved, "peak": NVLINK_PEER_GBS,
                 "unit": "GB/s", "frac": achieved / NVLINK_PEER_GBS,

@@ -271,14 +271,17 @@ int fp8lm_adam_step_delayed(fp8lm_plan* plan, const uint8_t* g8, const float* g_
  * (N = 1), so the quantize kernel also runs Adam pass 1 on them (4 launches per step,
  * 26 B/param instead of 27).  Mode P2P: the exchange kernel runs Adam pass 1 on the
  * elements of its own shard (1/N of pass 1 per rank) and combines the ranks' partial
- * state maxima through the pads; the all-gather (A5) is a PULL inside pass 2, which reads
- * each code from its owner's g8 window over NVLink while it streams the local states.
+ * state maxima through the pads; the all-gather (A5) is a PULL inside pass 2 (delayed
+ * state scaling: inside the single pass), which reads each code from its owner's g8
+ * window over NVLink while it streams the local states.
  * So after a P2P dp_step, g8 (this rank's window) holds the reduced codes of this
  * rank's shard [fp8lm_plan_shard_begin(rank), +shard bytes) only — every other result
  * (scales, sat, mu, the four states) is bit-identical to the three calls; use
  * fp8lm_grad_allreduce for a fully gathered g8.  Other modes: the three calls in sequence.
  * w_hist != NULL selects delayed state scaling (fp8lm_adam_step_delayed semantics); in
- * mode LOCAL the quantize kernel then also runs the single AdamW pass (20 B/param). */
+ * mode LOCAL the quantize kernel then also runs the single AdamW pass (20 B/param).
+ * Mode ZERO: the owner's pass 2 also broadcasts w8 (+ scalars) into every rank's window
+ * (JIT; delayed state scaling runs the three calls). */
 int fp8lm_dp_step(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
                   float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
                   float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,

@@ -283,6 +283,12 @@ int fp8lm_plan_destroy(fp8lm_plan* plan) {
   if (plan->win_g8) cudaFree(plan->win_g8);
   if (plan->win_pad) cudaFree(plan->win_pad);
   if (plan->win_w8) cudaFree(plan->win_w8);
+  for (cudaStream_t st : plan->ce_streams)
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : plan->ce_events)
+    if (ev) cudaEventDestroy(ev);
+  for (ShardItem* d : plan->ce_items) cudaFree(d);
+  if (plan->ce_recv) cudaFree(plan->ce_recv);
   if (plan->own) fp8lm_plan_destroy(plan->own);
   delete plan;
   return FP8LM_OK;
@@ -304,6 +310,73 @@ int32_t fp8lm_plan_owned_count(const fp8lm_plan* p) {
 }
 
 // ---------------------------------------------------------------- mode P2P windows
+// ---------------------------------------------------------------- copy-engine RS
+// Stream memory operations from the driver (no -lcuda: resolved through the runtime)
+typedef int (*StreamValue32Fn)(cudaStream_t, void*, uint32_t, unsigned int);
+static StreamValue32Fn g_write32 = nullptr, g_wait32 = nullptr;
+static bool stream_memops() {
+  static int ok = -1;
+  if (ok < 0) {
+    void *w = nullptr, *r = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    ok = cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+         cudaGetDriverEntryPoint("cuStreamWaitValue32", &r, cudaEnableDefault, &q2) == cudaSuccess &&
+         q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && r;
+    if (ok) {
+      g_write32 = reinterpret_cast<StreamValue32Fn>(w);
+      g_wait32 = reinterpret_cast<StreamValue32Fn>(r);
+    }
+    cudaGetLastError();
+  }
+  return ok == 1;
+}
+constexpr unsigned kWaitGeq = 0x0;       // CU_STREAM_WAIT_VALUE_GEQ (wrap-safe)
+constexpr unsigned kWriteFenced = 0x0;   // CU_STREAM_WRITE_VALUE_DEFAULT: system fence first
+
+// FP8LM_P2P_RS = "ce" (default) | "sm"; FP8LM_CE_CHUNKS = chunks per shard (1..16, default 4)
+static int ce_setup(fp8lm_plan* p) {
+  const char* mode = getenv("FP8LM_P2P_RS");
+  if ((mode && strcmp(mode, "sm") == 0) || !stream_memops()) return FP8LM_OK;
+  int C = 4;
+  if (const char* e = getenv("FP8LM_CE_CHUNKS")) C = atoi(e);
+  if (C <= 0) return FP8LM_OK;
+  C = std::min(C, kMaxCeChunks);
+  const int N = p->nranks;
+  const int64_t S_ = p->shard;
+  p->ce_chunk = std::max<int64_t>(round_up((S_ + C - 1) / C, 64), 64);
+  C = (int)((S_ + p->ce_chunk - 1) / p->ce_chunk);
+  CUDA_TRY(cudaMalloc(&p->ce_recv, (size_t)S_ * N));
+  p->ce_streams.resize(N, nullptr);
+  p->ce_events.resize(N + 1, nullptr);
+  CUDA_TRY(cudaEventCreateWithFlags(&p->ce_events[0], cudaEventDisableTiming));
+  for (int q = 0; q < N; ++q) {
+    if (q == p->rank) continue;
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->ce_streams[q], cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ce_events[1 + q], cudaEventDisableTiming));
+  }
+  // per chunk: the work items of the quantize (every shard's chunk c), clipped
+  for (int c = 0; c < C; ++c) {
+    std::vector<ShardItem> v;
+    for (const ShardItem& it : p->items) {
+      for (int k = 0; k < N; ++k) {
+        const int64_t lo = k * S_ + c * p->ce_chunk;
+        const int64_t hi = std::min(lo + p->ce_chunk, (int64_t)(k + 1) * S_);
+        const int64_t a = std::max(lo, it.pos), b = std::min(hi, it.pos + (int64_t)it.len);
+        if (a < b) v.push_back(ShardItem{a, it.t, (int32_t)(b - a)});
+      }
+    }
+    std::sort(v.begin(), v.end(), [](const ShardItem& x, const ShardItem& y) { return x.pos < y.pos; });
+    ShardItem* d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, sizeof(ShardItem) * std::max<size_t>(v.size(), 1)));
+    if (!v.empty())
+      CUDA_TRY(cudaMemcpy(d, v.data(), sizeof(ShardItem) * v.size(), cudaMemcpyHostToDevice));
+    p->ce_items.push_back(d);
+    p->ce_nitems.push_back((int64_t)v.size());
+  }
+  p->ce_chunks = C;
+  return FP8LM_OK;
+}
+
 int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
   if (!p || (p->mode != FP8LM_MODE_P2P && p->mode != FP8LM_MODE_ZERO))
     return fail(FP8LM_EINVAL, "peer_setup: plan mode is not P2P / ZERO");
@@ -360,12 +433,18 @@ int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
     tab.pad[q] = static_cast<uint32_t*>(pp);
     tab.w8[q] = static_cast<uint8_t*>(pw);
   }
+  p->peer_send.assign(tab.send, tab.send + N);
+  p->peer_pad.assign(tab.pad, tab.pad + N);
   CUDA_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(p->win_pad) + kPadTable, &tab, sizeof tab,
                       cudaMemcpyHostToDevice));
   // (every peer zeroed its pad before contributing its handles to the all-gather above,
   // so no signal can land in an uninitialised pad)
   p->dev.send = p->win_send;
   p->p2p_ready = true;
+  if (p->mode == FP8LM_MODE_P2P && N > 1) {
+    int rc = ce_setup(p);
+    if (rc) return rc;
+  }
   return FP8LM_OK;
 #else
   (void)comm; (void)stream;
@@ -860,7 +939,7 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
   const bool delayed = w_hist != nullptr;
   if (delayed && (hist_slot < 0 || hist_slot >= 16)) return fail(FP8LM_EINVAL, "dp_step: hist_slot not in [0, 16)");
   if ((p->mode != FP8LM_MODE_LOCAL && p->mode != FP8LM_MODE_P2P && p->mode != FP8LM_MODE_ZERO) ||
-      p->T == 0 || (delayed && p->mode != FP8LM_MODE_LOCAL)) {
+      p->T == 0 || (delayed && p->mode == FP8LM_MODE_ZERO)) {
     rc = fp8lm_grad_allreduce(p, comm, grads, src_dtype, s_g, skip, g8, g_scale, g_scale_inv, sat,
                               mu, stream);
     if (rc) return rc;
@@ -911,15 +990,58 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
     int nsrc = 0;
     if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
-    uint8_t* dst[1] = {p->win_send};
-    CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
-    // the exchange leaves each rank's reduced shard in its own window; pass 2 pulls the
-    // other shards' codes from the peers' windows (the all-gather, overlapped with pass 2)
-    const P2PArgs x = p2p_args(p, p->epoch);
-    CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip,
-                                  S(stream)));
-    // pass 2 starts its work order at this rank's shard: the ranks pull from different
-    // owners at any moment instead of all from one (FP8LM_PULL_ROT=0 disables, diagnosis)
+    P2PArgs x = p2p_args(p, p->epoch);
+    if (p->ce_chunks > 0) {
+      // copy-engine reduce-scatter: the quantize runs in chunks; after each, a stream
+      // write tells every peer that its part of the chunk is in this send window, and
+      // one copy-engine stream per peer copies the peer's codes of this rank's shard
+      // chunk into recv as soon as the peer's signal arrives — the NVLink transfer runs
+      // under the quantize of the later chunks instead of inside the exchange kernel
+      cudaStream_t s = S(stream);
+      const int N = p->nranks, me = p->rank;
+      const uint32_t eq = ++p->epoch_q;
+      CUDA_TRY(cudaEventRecord(p->ce_events[0], s));     // recv is free after the last step
+      for (int q = 0; q < N; ++q)
+        if (q != me) CUDA_TRY(cudaStreamWaitEvent(p->ce_streams[q], p->ce_events[0], 0));
+      for (int c = 0; c < p->ce_chunks; ++c) {
+        DevPlan dc = p->dev;
+        dc.items = p->ce_items[c];
+        dc.n_items = p->ce_nitems[c];
+        uint8_t* dst[1] = {p->win_send};
+        CUDA_TRY(launch_quantize(dc, srcs, dst, 1, src_dtype, s_g, nullptr, s));
+        for (int q = 0; q < N; ++q) {
+          if (q == me) continue;
+          void* flag = reinterpret_cast<uint8_t*>(p->peer_pad[q]) + kPadFlagQ + 4 * (c * kMaxPeers + me);
+          if (g_write32(s, flag, eq, kWriteFenced) != 0) return fail(FP8LM_ECUDA, "cuStreamWriteValue32 failed");
+        }
+        const int64_t off = c * p->ce_chunk;
+        const int64_t len = std::min(p->ce_chunk, p->shard - off);
+        for (int q = 0; q < N; ++q) {
+          if (q == me) continue;
+          void* flag = reinterpret_cast<uint8_t*>(p->win_pad) + kPadFlagQ + 4 * (c * kMaxPeers + q);
+          if (g_wait32(p->ce_streams[q], flag, eq, kWaitGeq) != 0) return fail(FP8LM_ECUDA, "cuStreamWaitValue32 failed");
+          ProfScope ps_(P_CE_RS, p->ce_streams[q]);
+          CUDA_TRY(cudaMemcpyAsync(p->ce_recv + q * p->shard + off, p->peer_send[q] + me * p->shard + off,
+                                   (size_t)len, cudaMemcpyDeviceToDevice, p->ce_streams[q]));
+        }
+      }
+      for (int q = 0; q < N; ++q) {
+        if (q == me) continue;
+        CUDA_TRY(cudaEventRecord(p->ce_events[1 + q], p->ce_streams[q]));
+        CUDA_TRY(cudaStreamWaitEvent(s, p->ce_events[1 + q], 0));
+      }
+      x.ce_recv = p->ce_recv;
+      x.ce_stride = p->shard;
+      x.ce_lo = p->shard * me;
+    } else {
+      uint8_t* dst[1] = {p->win_send};
+      CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
+    }
+    // the exchange leaves each rank's reduced shard in its own window; the AdamW pass
+    // that encodes the states pulls the other shards' codes from the peers' windows (the
+    // all-gather, overlapped with its HBM traffic), walking its work items from this
+    // rank's shard on so that the ranks pull from different owners at any moment
+    // (FP8LM_PULL_ROT=0 disables the rotation, diagnosis)
     static const bool rotate = !getenv("FP8LM_PULL_ROT") || atoi(getenv("FP8LM_PULL_ROT")) != 0;
     const int64_t lo = p->shard * p->rank;
     const auto first = std::lower_bound(p->items.begin(), p->items.end(), lo,
@@ -928,6 +1050,14 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
     ext.pull_tab = x.tab;
     ext.pull_shard = p->shard;
     ext.rot = rotate ? (int64_t)(first - p->items.begin()) : 0;
+    if (delayed) {            // reduce-scatter only, then the single delayed pass
+      CUDA_TRY(launch_reduce_p2p(p->dev, x, g8, s_g, tail, S(stream), /*ag=*/false));
+      CUDA_TRY(launch_adam_delayed(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip,
+                                   w_hist, hist_slot, S(stream), &ext));
+      return FP8LM_OK;
+    }
+    CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip,
+                                  S(stream)));
     CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream),
                          /*pass1=*/false, &ext));
     return FP8LM_OK;

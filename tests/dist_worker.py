@@ -110,7 +110,7 @@ def main():
         for t in range(plan.T):
             p = res["per_tensor"][t]
             sl = slice(plan.offsets[t], plan.offsets[t] + plan.numels[t])
-            if g8 is not None and args.mode == "p2p" and not args.unfused and not args.delayed:
+            if g8 is not None and args.mode == "p2p" and not args.unfused:
                 # fused P2P step: the all-gather is pulled inside pass 2, so this rank's
                 # window holds its own shard's codes only (include/fp8lm.h, fp8lm_dp_step)
                 lo, hi = plan.shard_begin(rank), plan.shard_begin(rank) + plan.shard_bytes
