@@ -289,6 +289,9 @@ int fp8lm_plan_destroy(fp8lm_plan* plan) {
     if (ev) cudaEventDestroy(ev);
   for (ShardItem* d : plan->ce_items) cudaFree(d);
   if (plan->ce_recv) cudaFree(plan->ce_recv);
+  if (plan->qx.qitems) cudaFree(const_cast<ShardItem*>(plan->qx.qitems));
+  if (plan->qx.pitems) cudaFree(const_cast<ShardItem*>(plan->qx.pitems));
+  if (plan->qx.ctr) cudaFree(plan->qx.ctr);
   if (plan->own) fp8lm_plan_destroy(plan->own);
   delete plan;
   return FP8LM_OK;
@@ -381,6 +384,53 @@ static int ce_setup(fp8lm_plan* p) {
   return FP8LM_OK;
 }
 
+// FP8LM_P2P_QX = chunks of the quantize + exchange pipeline (k_qx; 0 = off: quantize, then
+// the exchange kernel)
+static int qx_setup(fp8lm_plan* p) {
+  int C = 0;
+  if (const char* e = getenv("FP8LM_P2P_QX")) C = atoi(e);
+  if (C <= 0 || p->ce_chunks > 0) return FP8LM_OK;
+  C = std::min(C, kMaxCeChunks);
+  const int N = p->nranks, me = p->rank;
+  const int64_t S_ = p->shard;
+  const int64_t Sc = std::max<int64_t>(round_up((S_ + C - 1) / C, 64), 64);
+  C = (int)((S_ + Sc - 1) / Sc);
+  std::vector<ShardItem> q, pi;
+  QxHost& h = p->qx;
+  for (int c = 0; c < C; ++c) {
+    h.qoff[c] = (int64_t)q.size();
+    h.poff[c] = (int64_t)pi.size();
+    std::vector<ShardItem> v;
+    for (const ShardItem& it : p->items) {
+      for (int k = 0; k < N; ++k) {
+        const int64_t lo = k * S_ + c * Sc, hi = std::min(lo + Sc, (int64_t)(k + 1) * S_);
+        const int64_t a = std::max(lo, it.pos), b = std::min(hi, it.pos + (int64_t)it.len);
+        if (a < b) v.push_back(ShardItem{a, it.t, (int32_t)(b - a)});
+      }
+    }
+    std::sort(v.begin(), v.end(), [](const ShardItem& x, const ShardItem& y) { return x.pos < y.pos; });
+    q.insert(q.end(), v.begin(), v.end());
+    const int64_t lo = me * S_ + c * Sc, hi = std::min(lo + Sc, (int64_t)(me + 1) * S_);
+    for (const ShardItem& it : p->shard_items) {
+      const int64_t a = std::max(lo, it.pos), b = std::min(hi, it.pos + (int64_t)it.len);
+      if (a < b) pi.push_back(ShardItem{a, it.t, (int32_t)(b - a)});
+    }
+  }
+  h.qoff[C] = (int64_t)q.size();
+  h.poff[C] = (int64_t)pi.size();
+  ShardItem *dq = nullptr, *dp = nullptr;
+  CUDA_TRY(cudaMalloc(&dq, sizeof(ShardItem) * std::max<size_t>(q.size(), 1)));
+  CUDA_TRY(cudaMalloc(&dp, sizeof(ShardItem) * std::max<size_t>(pi.size(), 1)));
+  if (!q.empty()) CUDA_TRY(cudaMemcpy(dq, q.data(), sizeof(ShardItem) * q.size(), cudaMemcpyHostToDevice));
+  if (!pi.empty()) CUDA_TRY(cudaMemcpy(dp, pi.data(), sizeof(ShardItem) * pi.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&h.ctr, sizeof(uint32_t) * kMaxCeChunks));
+  CUDA_TRY(cudaMemset(h.ctr, 0, sizeof(uint32_t) * kMaxCeChunks));
+  h.qitems = dq;
+  h.pitems = dp;
+  h.C = C;
+  return FP8LM_OK;
+}
+
 int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
   if (!p || (p->mode != FP8LM_MODE_P2P && p->mode != FP8LM_MODE_ZERO))
     return fail(FP8LM_EINVAL, "peer_setup: plan mode is not P2P / ZERO");
@@ -448,6 +498,7 @@ int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
   if (p->mode == FP8LM_MODE_P2P && N > 1) {
     int rc = ce_setup(p);
     if (rc) return rc;
+    if ((rc = qx_setup(p))) return rc;
   }
   return FP8LM_OK;
 #else
@@ -1037,7 +1088,7 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
       x.ce_recv = p->ce_recv;
       x.ce_stride = p->shard;
       x.ce_lo = p->shard * me;
-    } else {
+    } else if (p->qx.C == 0 || delayed) {   // (k_qx quantizes inside the exchange)
       uint8_t* dst[1] = {p->win_send};
       CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
     }
@@ -1060,8 +1111,13 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
                                    w_hist, hist_slot, S(stream), &ext));
       return FP8LM_OK;
     }
-    CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip,
-                                  S(stream)));
+    if (p->qx.C > 0 && p->ce_chunks == 0) {
+      CUDA_TRY(launch_qx(p->dev, x, s_g, tail, g8, srcs[0], src_dtype, *m1, *v, *master, *w8, *hp,
+                         skip, p->qx, S(stream)));
+    } else {
+      CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip,
+                                    S(stream)));
+    }
     CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream),
                          /*pass1=*/false, &ext));
     return FP8LM_OK;

@@ -124,6 +124,16 @@ struct Pass2Ext {
   int T_full = 0;
 };
 
+// quantize + exchange pipeline of the P2P dp_step (k_qx): host view of the chunk tables
+struct QxHost {
+  const ShardItem* qitems = nullptr;   // device
+  const ShardItem* pitems = nullptr;   // device
+  int64_t qoff[kMaxCeChunks + 1] = {};
+  int64_t poff[kMaxCeChunks + 1] = {};
+  int C = 0;
+  uint32_t* ctr = nullptr;             // device [kMaxCeChunks], zero at rest
+};
+
 // outputs of the Eq. 6 / mu tail of fp8lm_grad_allreduce
 struct TailArgs {
   int nranks;
@@ -177,6 +187,8 @@ struct fp8lm_plan {
   std::vector<fp8lm::ShardItem*> ce_items;   // device: per chunk, the clipped quantize items
   std::vector<int64_t> ce_nitems;
   uint32_t epoch_q = 0;
+  // quantize + exchange pipeline (k_qx, FP8LM_P2P_QX): chunk tables owned by the plan
+  fp8lm::QxHost qx;
   // mode ZERO: Alg. 1 owners, the owned tensors and the compact sub-plan over them
   std::vector<int32_t> owner, own2full;
   std::vector<int64_t> own_gpos, full2own_off;
@@ -194,7 +206,7 @@ enum ProfId : int {
   P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
   P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_W8_BCAST, P_ADAM_DELAYED,
   P_QADAM_DELAYED, P_STRAT_AMAX, P_STRAT_REDUCE, P_SP_ALLGATHER, P_SP_REDUCE_SCATTER, P_CE_RS,
-  P_COUNT
+  P_QX, P_COUNT
 };
 bool prof_on();
 struct ProfScope {
@@ -244,6 +256,10 @@ cudaError_t launch_adam_delayed(const DevPlan& p, const uint8_t* g8, const float
                                 const fp8lm_adam_hp& hp, const int32_t* skip, float* w_hist,
                                 int hist_slot, cudaStream_t s, const Pass2Ext* ext = nullptr);
 // mode P2P fused step: exchange + reduce + Adam pass 1 on the own shard (+ maxima exchange)
+cudaError_t launch_qx(const DevPlan& p, const P2PArgs& x, const float* s_g, const TailArgs& tail,
+                      uint8_t* g8, const void* grads, int src_dtype, const fp8lm_stensors& m1,
+                      const fp8lm_stensors& v, const fp8lm_stensors& w, const fp8lm_stensors& w8,
+                      const fp8lm_adam_hp& hp, const int32_t* skip, const QxHost& q, cudaStream_t s);
 cudaError_t launch_reduce_p2p_a1(const DevPlan& p, const P2PArgs& x, const float* s_g,
                                  const TailArgs& tail, uint8_t* g8, const fp8lm_stensors& m1,
                                  const fp8lm_stensors& v, const fp8lm_stensors& w,
