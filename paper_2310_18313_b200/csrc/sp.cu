@@ -7,13 +7,14 @@
 // path.  Every op is ONE cooperative kernel in three phases separated by grid barriers:
 //   1  local amax -> s_r; the last CTA publishes s_r into every rank's pad, waits for all
 //      ranks and takes the MIN (Eq. 4)
-//   2  all-gather: quantize the local partition and STORE the codes into every rank's
-//      receive window (push); reduce-scatter: quantize the full local gradient into the
-//      own send window; the last CTA releases "data" to every rank, all CTAs wait for
-//      every rank's "data"
-//   3  all-gather: copy the gathered codes and / or dequantize them into the caller's
-//      buffers; reduce-scatter: LOAD chunk `rank` from every rank's send window, sum in
-//      rank order in binary32, fl(S * fl(1/s)) -> out
+//   2  all-gather: quantize the local partition into the own receive window at
+//      rank * m; reduce-scatter: quantize the full local gradient into the own send
+//      window; the last CTA releases "data" to every rank, all CTAs wait for every
+//      rank's "data"
+//   3  all-gather: LOAD rank r's codes from rank r's receive window (pull over NVLink)
+//      and copy them out and / or dequantize them into the caller's buffers;
+//      reduce-scatter: LOAD chunk `rank` from every rank's send window, sum in rank
+//      order in binary32, fl(S * fl(1/s)) -> out
 // Flags carry the op's epoch (host counter, identical on every rank): "scale" (s_r
 // published), "data" (codes stored / quantized) and "done" (this rank no longer reads
 // its receive window / peers' send windows for that epoch), each one u32 per source
@@ -231,29 +232,23 @@ __device__ __forceinline__ void phase_quant(const T* __restrict__ x, int64_t n, 
   const float s = __uint_as_float(*(volatile uint32_t*)(a.scratch + kSpScrS));
   const int64_t dst_off = PUSH ? (int64_t)a.rank * n : 0;
   uint8_t* own_send = P.send[0];
+  uint8_t* own_recv = P.recv[0];
 #pragma unroll
-  for (int q = 1; q < NR; ++q) if (q == a.rank) own_send = P.send[q];
+  for (int q = 1; q < NR; ++q)
+    if (q == a.rank) { own_send = P.send[q]; own_recv = P.recv[q]; }
   const int64_t ng = a.vec ? n / 16 : 0;
   for (int64_t gi = cta_lo(ng) + threadIdx.x, e = cta_hi(ng); gi < e; gi += kSpT) {
     float v[16];
     In<T>::get16(x, gi * 16, v);
     const uint4 c = quant16(v, s);
-    if (PUSH) {
-#pragma unroll
-      for (int q = 0; q < NR; ++q) st128(P.recv[q] + dst_off + gi * 16, c);
-    } else {
-      st128(own_send + gi * 16, c);
-    }
+    if (PUSH) st128(own_recv + dst_off + gi * 16, c);   // all-gather: pulled by the peers
+    else st128(own_send + gi * 16, c);
   }
   const int64_t t0 = ng * 16;
   for (int64_t i = t0 + cta_lo(n - t0) + threadIdx.x, e = t0 + cta_hi(n - t0); i < e; i += kSpT) {
     const uint8_t c = (uint8_t)(e4m3x2(__fmul_rn(In<T>::get(x, i), s), 0.0f) & 0xFFu);
-    if (PUSH) {
-#pragma unroll
-      for (int q = 0; q < NR; ++q) P.recv[q][dst_off + i] = c;
-    } else {
-      own_send[i] = c;
-    }
+    if (PUSH) own_recv[dst_off + i] = c;
+    else own_send[i] = c;
   }
   grid_phase(a, kSpScrTicketB, kSpScrFlag2, true, [&] { release_all<NR>(P, kSpPadFlagData, a.rank, a.epoch); });
   if (threadIdx.x == 0) wait_epoch(sp_flags(a.pad, kSpPadFlagData), NR, a.epoch);
@@ -268,27 +263,38 @@ __global__ void __launch_bounds__(kSpT) k_sp_allgather(const T* __restrict__ x, 
   phase_scale<T, NR>(x, m, a, P, scale_out);
   phase_quant<T, NR, true>(x, m, a, P);
   // phase 3: every rank's codes have landed: copy them out and / or dequantize
+  // PULL: rank r's codes are read straight from rank r's receive window (NVLink), so
+  // the transfer and the dequantize are one pass instead of a push followed by a read
   const float sinv = __uint_as_float(*(volatile uint32_t*)(a.scratch + kSpScrSinv));
   const int64_t total = m * NR;
-  const uint8_t* src = P.recv[0];
-#pragma unroll
-  for (int q = 1; q < NR; ++q) if (q == a.rank) src = P.recv[q];
   if (codes_out || out) {
     const int64_t ng = a.vec ? total / 16 : 0;
-    for (int64_t gi = cta_lo(ng) + threadIdx.x, e = cta_hi(ng); gi < e; gi += kSpT) {
-      const uint4 c = ld128_nc(src + gi * 16);
-      if (codes_out) st128(codes_out + gi * 16, c);
-      if (out) {
-        float d[16];
-        dec_e4m3x4(c.x, d); dec_e4m3x4(c.y, d + 4); dec_e4m3x4(c.z, d + 8); dec_e4m3x4(c.w, d + 12);
+    const int64_t gm = m / 16;                       // groups per rank (vector path)
+    constexpr int U = 4;                             // 16-byte peer loads in flight
+    for (int64_t g0 = cta_lo(ng) + threadIdx.x, e = cta_hi(ng); g0 < e; g0 += (int64_t)kSpT * U) {
+      uint4 c[U];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) d[k] = __fmul_rn(d[k], sinv);
-        Out<O>::put16(out, gi * 16, d);
+      for (int u = 0; u < U; ++u) {
+        const int64_t gi = g0 + (int64_t)u * kSpT;
+        if (gi < e) c[u] = ld128_peer(P.recv[(int)(gi / gm)] + gi * 16);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t gi = g0 + (int64_t)u * kSpT;
+        if (gi >= e) continue;
+        if (codes_out) st128(codes_out + gi * 16, c[u]);
+        if (out) {
+          float d[16];
+          dec_e4m3x4(c[u].x, d); dec_e4m3x4(c[u].y, d + 4); dec_e4m3x4(c[u].z, d + 8); dec_e4m3x4(c[u].w, d + 12);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) d[k] = __fmul_rn(d[k], sinv);
+          Out<O>::put16(out, gi * 16, d);
+        }
       }
     }
     const int64_t t0 = ng * 16;
     for (int64_t i = t0 + cta_lo(total - t0) + threadIdx.x, e = t0 + cta_hi(total - t0); i < e; i += kSpT) {
-      const uint8_t c = src[i];
+      const uint8_t c = P.recv[(int)(i / m)][i];
       if (codes_out) codes_out[i] = c;
       if (out) {
         float d, u;
