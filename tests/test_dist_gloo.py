@@ -1,4 +1,4 @@
-"""N > 1 host logic on CPU (world_size 2 and 3, gloo): the NCCL-mode data flow of
+"""N > 1 host logic on CPU (world_size 2, 3 and 8, gloo): the NCCL-mode data flow of
 fp8lm_amax_scale_sync / fp8lm_grad_allreduce — MIN all-reduce of the local scales
 (Eq. 4), the flat code buffer split into N shards by the library's plan (all-to-all
 transport), rank-order reduction of the own shard, in-place all-gather, summed
@@ -104,7 +104,7 @@ def _worker(rank, world, port, q):
         q.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_nccl_mode_protocol_matches_n_rank_oracle(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -204,7 +204,7 @@ def _pull_worker(rank, world, port, q):
         q.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_p2p_pull_allgather_matches_n_rank_oracle(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
