@@ -172,6 +172,18 @@ def test_local_fused_skip_and_screen_fallback(B):
     _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=3, specials=specials, lr=0.05)
 
 
+@pytest.mark.parametrize("fused,delayed", [(True, False), (False, False), (True, True)],
+                         ids=["dp_step", "three_calls", "delayed"])
+def test_local_tiny_moments_range_certificate(B, fused, delayed):
+    """Tensors whose m' / v' can leave the branch-free sqrt / division cores' range
+    (|m'| < 2^-60, 0 < v' < 2^-101: gradients of 1e-20 / 1e-30 / 1e-38) next to ordinary
+    ones: the per-tensor a-priori certificate (kernels.cu range_cert) fails for the tiny
+    ones, whose groups take the checked body with the exact intrinsics, and holds for the
+    others, which skip the per-element checks."""
+    amp = [1.0, 1e-20, 1e-30, 1e-12, 1e-3, 1e-38, 1.0, 1e-15, 1e-20]
+    _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=3, amp=amp, fused=fused, delayed=delayed)
+
+
 @pytest.mark.parametrize("N", [2, 3, 8])
 def test_simulated_ranks_multistep(B, N):
     """N simulated ranks on one device (config C1 protocol): RS+AG degenerate to a local
