@@ -56,16 +56,32 @@ def needs_rebuild() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Each source compiles to an object in parallel (kernels.cu dominates), then one link."""
     if not force and not needs_rebuild():
         return LIB
     inc, lib = nccl_dirs()
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
-           "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
-           "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared",
-           "-I", os.path.join(ROOT, "include")]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
+             "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
+             "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-I", os.path.join(ROOT, "include")]
     if inc:
-        cmd += ["-DFP8LM_WITH_NCCL", "-I", inc]
-    cmd += sources()
+        flags += ["-DFP8LM_WITH_NCCL", "-I", inc]
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *flags, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd))
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src} ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(sources())) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    cmd = [nvcc(), *ARCH, "-shared", *objs]
     if lib:
         cmd += ["-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
     cmd += ["-o", LIB + ".tmp"]
@@ -73,7 +89,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         print(" ".join(cmd))
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+        raise RuntimeError(f"nvcc link failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

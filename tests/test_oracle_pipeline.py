@@ -167,3 +167,39 @@ def test_nan_amax_reported():
     a, f = P.amax(np.array([-3.0, np.inf], np.float32))
     assert np.isinf(a) and f
     assert P.amax(np.zeros(0, np.float32)) == (0.0, False)
+
+
+def test_worked_example_adam_half_through_train_step():
+    """SURVEY §8(c) worked example, Adam half, through oracle.step.train_step's non-skip
+    path (dequantize -> adam_step hand-off): u, w', s_m = 2986666.25, m1 codes
+    [0x7E, 0xE9, 0x7A, 0x38] and the v / master / w8 codes and scales, each derived by
+    hand in tests/golden/worked_example.json _derivation_adam (P:172-178 state layout,
+    P:301 hyper-parameters).  Passing scale instead of scale_inv, dequantizing the
+    per-rank codes, or skipping Adam changes every one of them."""
+    w = json.load(open(os.path.join(GOLD, "worked_example.json")))
+    a = w["adam"]
+    g0 = np.array(w["g0"], np.float32)
+    g1 = np.array(w["g1"], np.float32)
+    st0 = A.init_state(np.array(a["w0"], np.float32))
+    assert st0.master.codes.tolist() == a["master0_codes"]
+    r = S.train_step([[g0], [g1]], [F32(1.0)], [st0], A.hyper_params(a["lr"], a["step"]))
+    assert not r["skip"]
+    ad = r["per_tensor"][0]["adam"]
+    assert ad["m"].tolist() == [float(F32(x)) for x in a["m_new"]]
+    assert ad["v"].tolist() == [float(F32(x)) for x in a["v_new"]]
+    assert ad["w"].tolist() == [float(F32(x)) for x in a["w_new"]]
+    ns = r["states"][0]
+    hx = lambda v: "0x%08X" % np.float32(v).view(np.uint32)
+    assert ns.m1.scale == F32(a["s_m"])
+    assert hx(ns.v.scale) == a["s_v_hex"]
+    assert hx(ns.master.scale) == a["s_w_hex"]
+    assert hx(ns.w8.scale) == a["s_8_hex"]
+    assert ns.m1.codes.tolist() == a["m1_codes"]
+    assert ns.v.codes.tolist() == a["v_codes"]
+    assert ns.master.codes.tolist() == a["master_codes"]
+    assert ns.w8.codes.tolist() == a["w8_codes"]
+    # u follows from w' and the master's decoded w: fl(w*decay) - fl(step*u) = w' exactly
+    hp = A.hyper_params(a["lr"], a["step"])
+    u = np.array(a["u"], np.float32)
+    wd = st0.master.value() * hp.decay
+    assert ((wd - hp.step_size * u).astype(np.float32) == ad["w"]).all()
