@@ -167,6 +167,30 @@ int32_t fp8lm_plan_owned_count(const fp8lm_plan* plan);
  * Synchronous.  EINVAL unless mode == P2P and comm matches the plan; ECUDA / ENCCL on
  * failure. */
 int fp8lm_peer_setup(fp8lm_plan* plan, fp8lm_comm* comm, void* stream);
+/* Single-process loopback of modes P2P / ZERO (tests, and any host that drives several
+ * logical ranks on one GPU): plans[r] (r = 0..n-1) are n bound plans of one process,
+ * created with the same numels and mode (P2P or ZERO), nranks = n and rank = r.  Each
+ * gets its windows as in fp8lm_peer_setup, but the peer table points at the other
+ * plans' local windows (no IPC, no communicator).  The ranks then run the same call
+ * sequence, each on its OWN stream (the kernels meet at the same flags as over NVLink,
+ * so the n ranks' launches must be able to run concurrently); every kernel of a
+ * loopback plan launches at most floor(#SMs / n) CTAs and without the cooperative / PDL
+ * attributes, so that all ranks' kernels are resident together.  Same arithmetic and
+ * bit-identical results as n processes; not a performance configuration.  Synchronous.
+ * EINVAL on mismatched plans or a plan already set up. */
+int fp8lm_peer_setup_loopback(fp8lm_plan* const* plans, int32_t n, void* stream);
+
+/* Peer-wait watchdog (modes P2P / ZERO and the SP converter).  The kernels that meet
+ * other ranks spin on epoch flags in the peers' pads.  A flag still behind its epoch
+ * after `seconds` (default 600: a peer may save a checkpoint or evaluate between steps)
+ * makes the waiting kernel record {1, flag index, epoch wanted, value seen} in a
+ * host-mapped report and trap (a sticky CUDA error: the job must restart, as after an
+ * NCCL timeout).  seconds = 0: wait forever.  Applies to kernels launched after the
+ * call; EINVAL on a negative / non-finite value.  fp8lm_peer_timeout_report copies the
+ * report (all zero if no wait timed out); readable after the trap. */
+int fp8lm_set_peer_timeout(double seconds);
+int fp8lm_peer_timeout_report(uint32_t* out4);
+
 /* Mode P2P: this rank's g8 window (device); pass it as g8 to the calls below.  NULL if
  * fp8lm_peer_setup has not run. */
 uint8_t* fp8lm_peer_g8(const fp8lm_plan* plan);
@@ -368,7 +392,8 @@ int fp8lm_allreduce_strategy(int32_t strategy, const float* grads, int32_t nrank
  * the fp8lm_sp object), no NCCL call on the data path; 1 B per element crosses NVLink
  * instead of 2 for bf16.  Every call is COLLECTIVE: all ranks call the same sequence of
  * ops with the same m (ops are matched by a per-object counter), asynchronous on
- * `stream`; a rank that never arrives makes the others trap after 20 s.
+ * `stream`; a rank that never arrives makes the others trap after the peer-wait
+ * watchdog timeout (fp8lm_set_peer_timeout, default 600 s).
  *
  * fp8lm_sp_create: collective over comm (NULL = a single rank, no peers); max_elems
  * bounds N*m of every later op.  Allocates two windows of max_elems bytes and a 512-byte

@@ -70,6 +70,9 @@ _sig("fp8lm_plan_shard_begin", _i64, _p, _i32)
 _sig("fp8lm_plan_workspace_bytes", C.c_size_t, _p)
 _sig("fp8lm_plan_bind", C.c_int, _p, _p, C.c_size_t, _p)
 _sig("fp8lm_peer_setup", C.c_int, _p, _p, _p)
+_sig("fp8lm_peer_setup_loopback", C.c_int, C.POINTER(_p), _i32, _p)
+_sig("fp8lm_set_peer_timeout", C.c_int, _f64)
+_sig("fp8lm_peer_timeout_report", C.c_int, C.POINTER(C.c_uint32))
 _sig("fp8lm_peer_g8", _p, _p)
 _sig("fp8lm_peer_w8", _p, _p)
 _sig("fp8lm_peer_w8_scalars", _p, _p)
@@ -241,9 +244,14 @@ class Plan:
             lib.fp8lm_plan_destroy(h)
             self.handle = None
 
+    peer_ready = False
+
     def peer_setup(self, comm: "Comm", stream=None):
         """Mode P2P: map every rank's windows (collective; see fp8lm_peer_setup)."""
+        if self.peer_ready:
+            return
         _check(lib.fp8lm_peer_setup(self.handle, comm.handle, _stream(stream)), "fp8lm_peer_setup")
+        self.peer_ready = True
 
     def _window(self, ptr, n, typestr):
         if not ptr:
@@ -350,6 +358,28 @@ class OptimizerState:
 
     def tensors(self):
         return dict(m1=self.m1, v=self.v, master=self.master, w8=self.w8)
+
+
+def peer_setup_loopback(plans: Sequence[Plan], stream=None):
+    """fp8lm_peer_setup_loopback: plans[r] (mode P2P or ZERO, nranks = len(plans),
+    rank r) become the ranks of one single-process group on this GPU.  Each rank must then
+    run its calls on its own stream (the ranks' kernels meet at peer flags)."""
+    arr = (_p * len(plans))(*[p.handle.value for p in plans])
+    _check(lib.fp8lm_peer_setup_loopback(arr, len(plans), _stream(stream)), "fp8lm_peer_setup_loopback")
+    for p in plans:
+        p.peer_ready = True
+
+
+def set_peer_timeout(seconds: float):
+    """Peer-wait watchdog (fp8lm_set_peer_timeout): 0 = wait forever."""
+    _check(lib.fp8lm_set_peer_timeout(float(seconds)), "fp8lm_set_peer_timeout")
+
+
+def peer_timeout_report():
+    """-> (hit, flag index, epoch wanted, value seen) of the last watchdog trap, or zeros."""
+    out = (C.c_uint32 * 4)()
+    _check(lib.fp8lm_peer_timeout_report(out), "fp8lm_peer_timeout_report")
+    return tuple(out)
 
 
 # ------------------------------------------------------------------ the four calls
@@ -559,7 +589,7 @@ class FP8DataParallel:
         self.skip = torch.zeros(1, dtype=torch.int32, device=dev)
         self.layout = plan
         if plan.mode == MODE_P2P:
-            plan.peer_setup(comm)
+            plan.peer_setup(comm)       # no-op after peer_setup_loopback
             self.g8 = plan.peer_g8()
             self.comm = None            # the exchange runs in the library's kernels
         elif plan.mode == MODE_ZERO:

@@ -283,15 +283,6 @@ int fp8lm_plan_destroy(fp8lm_plan* plan) {
   if (plan->win_g8) cudaFree(plan->win_g8);
   if (plan->win_pad) cudaFree(plan->win_pad);
   if (plan->win_w8) cudaFree(plan->win_w8);
-  for (cudaStream_t st : plan->ce_streams)
-    if (st) cudaStreamDestroy(st);
-  for (cudaEvent_t ev : plan->ce_events)
-    if (ev) cudaEventDestroy(ev);
-  for (ShardItem* d : plan->ce_items) cudaFree(d);
-  if (plan->ce_recv) cudaFree(plan->ce_recv);
-  if (plan->qx.qitems) cudaFree(const_cast<ShardItem*>(plan->qx.qitems));
-  if (plan->qx.pitems) cudaFree(const_cast<ShardItem*>(plan->qx.pitems));
-  if (plan->qx.ctr) cudaFree(plan->qx.ctr);
   if (plan->own) fp8lm_plan_destroy(plan->own);
   delete plan;
   return FP8LM_OK;
@@ -313,121 +304,55 @@ int32_t fp8lm_plan_owned_count(const fp8lm_plan* p) {
 }
 
 // ---------------------------------------------------------------- mode P2P windows
-// ---------------------------------------------------------------- copy-engine RS
-// Stream memory operations from the driver (no -lcuda: resolved through the runtime)
-typedef int (*StreamValue32Fn)(cudaStream_t, void*, uint32_t, unsigned int);
-static StreamValue32Fn g_write32 = nullptr, g_wait32 = nullptr;
-static bool stream_memops() {
-  static int ok = -1;
-  if (ok < 0) {
-    void *w = nullptr, *r = nullptr;
-    cudaDriverEntryPointQueryResult q1, q2;
-    ok = cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
-         cudaGetDriverEntryPoint("cuStreamWaitValue32", &r, cudaEnableDefault, &q2) == cudaSuccess &&
-         q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && r;
-    if (ok) {
-      g_write32 = reinterpret_cast<StreamValue32Fn>(w);
-      g_wait32 = reinterpret_cast<StreamValue32Fn>(r);
-    }
-    cudaGetLastError();
-  }
-  return ok == 1;
-}
-constexpr unsigned kWaitGeq = 0x0;       // CU_STREAM_WAIT_VALUE_GEQ (wrap-safe)
-constexpr unsigned kWriteFenced = 0x0;   // CU_STREAM_WRITE_VALUE_DEFAULT: system fence first
-
-// FP8LM_P2P_RS = "sm" (default: the exchange kernel pulls the codes itself) | "ce";
-// FP8LM_CE_CHUNKS = chunks per shard (1..16, default 4).  Measured slower than "sm" on
-// B200 (GPT-125M N = 4: 0.82 vs 0.675 ms; GPT-7B N = 4: 37.4 vs 31.4 ms): the copy
-// engines reach ~400 GB/s of peer reads while the quantize streams HBM, so the copies
-// end long after the last chunk is quantized.
-static int ce_setup(fp8lm_plan* p) {
-  const char* mode = getenv("FP8LM_P2P_RS");
-  if (!mode || strcmp(mode, "ce") != 0 || !stream_memops()) return FP8LM_OK;
-  int C = 4;
-  if (const char* e = getenv("FP8LM_CE_CHUNKS")) C = atoi(e);
-  if (C <= 0) return FP8LM_OK;
-  C = std::min(C, kMaxCeChunks);
-  const int N = p->nranks;
-  const int64_t S_ = p->shard;
-  p->ce_chunk = std::max<int64_t>(round_up((S_ + C - 1) / C, 64), 64);
-  C = (int)((S_ + p->ce_chunk - 1) / p->ce_chunk);
-  CUDA_TRY(cudaMalloc(&p->ce_recv, (size_t)S_ * N));
-  p->ce_streams.resize(N, nullptr);
-  p->ce_events.resize(N + 1, nullptr);
-  CUDA_TRY(cudaEventCreateWithFlags(&p->ce_events[0], cudaEventDisableTiming));
-  for (int q = 0; q < N; ++q) {
-    if (q == p->rank) continue;
-    CUDA_TRY(cudaStreamCreateWithFlags(&p->ce_streams[q], cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&p->ce_events[1 + q], cudaEventDisableTiming));
-  }
-  // per chunk: the work items of the quantize (every shard's chunk c), clipped
-  for (int c = 0; c < C; ++c) {
-    std::vector<ShardItem> v;
-    for (const ShardItem& it : p->items) {
-      for (int k = 0; k < N; ++k) {
-        const int64_t lo = k * S_ + c * p->ce_chunk;
-        const int64_t hi = std::min(lo + p->ce_chunk, (int64_t)(k + 1) * S_);
-        const int64_t a = std::max(lo, it.pos), b = std::min(hi, it.pos + (int64_t)it.len);
-        if (a < b) v.push_back(ShardItem{a, it.t, (int32_t)(b - a)});
-      }
-    }
-    std::sort(v.begin(), v.end(), [](const ShardItem& x, const ShardItem& y) { return x.pos < y.pos; });
-    ShardItem* d = nullptr;
-    CUDA_TRY(cudaMalloc(&d, sizeof(ShardItem) * std::max<size_t>(v.size(), 1)));
-    if (!v.empty())
-      CUDA_TRY(cudaMemcpy(d, v.data(), sizeof(ShardItem) * v.size(), cudaMemcpyHostToDevice));
-    p->ce_items.push_back(d);
-    p->ce_nitems.push_back((int64_t)v.size());
-  }
-  p->ce_chunks = C;
+// this rank's symmetric windows (send, g8, w8, pad), zeroed where a peer may read first
+static int peer_alloc(fp8lm_plan* p) {
+  const size_t win = (size_t)p->g8_bytes;
+  const bool zero = p->mode == FP8LM_MODE_ZERO;
+  p->pad_bytes = pad_bytes_for(p->nranks, p->T);
+  CUDA_TRY(cudaMalloc(&p->win_send, win));
+  CUDA_TRY(cudaMalloc(&p->win_g8, zero ? 256 : win));     // ZERO: the owner's g8 is compact
+  CUDA_TRY(cudaMalloc(&p->win_w8, zero ? std::max<size_t>(p->total, 256) : 256));
+  CUDA_TRY(cudaMalloc(&p->win_pad, p->pad_bytes));
+  CUDA_TRY(cudaMemset(p->win_pad, 0, p->pad_bytes));
+  CUDA_TRY(cudaMemset(p->win_send, 0, win));
   return FP8LM_OK;
 }
 
-// FP8LM_P2P_QX = chunks of the quantize + exchange pipeline (k_qx; 0 = off: quantize, then
-// the exchange kernel)
-static int qx_setup(fp8lm_plan* p) {
-  int C = 0;
-  if (const char* e = getenv("FP8LM_P2P_QX")) C = atoi(e);
-  if (C <= 0 || p->ce_chunks > 0) return FP8LM_OK;
-  C = std::min(C, kMaxCeChunks);
-  const int N = p->nranks, me = p->rank;
-  const int64_t S_ = p->shard;
-  const int64_t Sc = std::max<int64_t>(round_up((S_ + C - 1) / C, 64), 64);
-  C = (int)((S_ + Sc - 1) / Sc);
-  std::vector<ShardItem> q, pi;
-  QxHost& h = p->qx;
-  for (int c = 0; c < C; ++c) {
-    h.qoff[c] = (int64_t)q.size();
-    h.poff[c] = (int64_t)pi.size();
-    std::vector<ShardItem> v;
-    for (const ShardItem& it : p->items) {
-      for (int k = 0; k < N; ++k) {
-        const int64_t lo = k * S_ + c * Sc, hi = std::min(lo + Sc, (int64_t)(k + 1) * S_);
-        const int64_t a = std::max(lo, it.pos), b = std::min(hi, it.pos + (int64_t)it.len);
-        if (a < b) v.push_back(ShardItem{a, it.t, (int32_t)(b - a)});
-      }
-    }
-    std::sort(v.begin(), v.end(), [](const ShardItem& x, const ShardItem& y) { return x.pos < y.pos; });
-    q.insert(q.end(), v.begin(), v.end());
-    const int64_t lo = me * S_ + c * Sc, hi = std::min(lo + Sc, (int64_t)(me + 1) * S_);
-    for (const ShardItem& it : p->shard_items) {
-      const int64_t a = std::max(lo, it.pos), b = std::min(hi, it.pos + (int64_t)it.len);
-      if (a < b) pi.push_back(ShardItem{a, it.t, (int32_t)(b - a)});
-    }
+static int peer_table_upload(fp8lm_plan* p, const PeerTable& tab) {
+  CUDA_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(p->win_pad) + kPadTable, &tab, sizeof tab,
+                      cudaMemcpyHostToDevice));
+  p->dev.send = p->win_send;
+  p->p2p_ready = true;
+  return FP8LM_OK;
+}
+
+// ---------------------------------------------------------------- peer-wait watchdog
+static uint32_t* g_report = nullptr;                 // host-mapped {hit, flag, epoch, seen}
+static unsigned long long g_timeout_ns = 600ull * 1000000000ull;
+
+static int watchdog_install() {
+  if (!g_report) {
+    void* h = nullptr;
+    CUDA_TRY(cudaHostAlloc(&h, 16, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(h, 0, 16);
+    g_report = static_cast<uint32_t*>(h);
   }
-  h.qoff[C] = (int64_t)q.size();
-  h.poff[C] = (int64_t)pi.size();
-  ShardItem *dq = nullptr, *dp = nullptr;
-  CUDA_TRY(cudaMalloc(&dq, sizeof(ShardItem) * std::max<size_t>(q.size(), 1)));
-  CUDA_TRY(cudaMalloc(&dp, sizeof(ShardItem) * std::max<size_t>(pi.size(), 1)));
-  if (!q.empty()) CUDA_TRY(cudaMemcpy(dq, q.data(), sizeof(ShardItem) * q.size(), cudaMemcpyHostToDevice));
-  if (!pi.empty()) CUDA_TRY(cudaMemcpy(dp, pi.data(), sizeof(ShardItem) * pi.size(), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMalloc(&h.ctr, sizeof(uint32_t) * kMaxCeChunks));
-  CUDA_TRY(cudaMemset(h.ctr, 0, sizeof(uint32_t) * kMaxCeChunks));
-  h.qitems = dq;
-  h.pitems = dp;
-  h.C = C;
+  uint32_t* dev = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), g_report, 0));
+  CUDA_TRY(wait_watchdog_set_kernels(g_timeout_ns, dev));
+  CUDA_TRY(wait_watchdog_set_sp(g_timeout_ns, dev));
+  return FP8LM_OK;
+}
+
+int fp8lm_set_peer_timeout(double seconds) {
+  if (!(seconds >= 0) || seconds > 1e9) return fail(FP8LM_EINVAL, "set_peer_timeout: bad seconds");
+  g_timeout_ns = (unsigned long long)(seconds * 1e9);
+  return watchdog_install();
+}
+
+int fp8lm_peer_timeout_report(uint32_t* out4) {
+  if (!out4) return fail(FP8LM_EINVAL, "peer_timeout_report: NULL");
+  for (int k = 0; k < 4; ++k) out4[k] = g_report ? reinterpret_cast<volatile uint32_t*>(g_report)[k] : 0u;
   return FP8LM_OK;
 }
 
@@ -440,15 +365,8 @@ int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
   if (!comm || comm->nranks != p->nranks || comm->rank != p->rank)
     return fail(FP8LM_EINVAL, "peer_setup: communicator does not match the plan");
   const int N = p->nranks;
-  const size_t win = (size_t)p->g8_bytes;
-  p->pad_bytes = pad_bytes_for(N, p->T);
-  const bool zero = p->mode == FP8LM_MODE_ZERO;
-  CUDA_TRY(cudaMalloc(&p->win_send, win));
-  CUDA_TRY(cudaMalloc(&p->win_g8, zero ? 256 : win));     // ZERO: the owner's g8 is compact
-  CUDA_TRY(cudaMalloc(&p->win_w8, zero ? std::max<size_t>(p->total, 256) : 256));
-  CUDA_TRY(cudaMalloc(&p->win_pad, p->pad_bytes));
-  CUDA_TRY(cudaMemset(p->win_pad, 0, p->pad_bytes));
-  CUDA_TRY(cudaMemset(p->win_send, 0, win));
+  int rc = watchdog_install();
+  if (rc || (rc = peer_alloc(p))) return rc;
   struct Handles { cudaIpcMemHandle_t send, g8, pad, w8; };
   Handles mine;
   CUDA_TRY(cudaIpcGetMemHandle(&mine.send, p->win_send));
@@ -487,24 +405,47 @@ int fp8lm_peer_setup(fp8lm_plan* p, fp8lm_comm* comm, void* stream) {
     tab.pad[q] = static_cast<uint32_t*>(pp);
     tab.w8[q] = static_cast<uint8_t*>(pw);
   }
-  p->peer_send.assign(tab.send, tab.send + N);
-  p->peer_pad.assign(tab.pad, tab.pad + N);
-  CUDA_TRY(cudaMemcpy(reinterpret_cast<uint8_t*>(p->win_pad) + kPadTable, &tab, sizeof tab,
-                      cudaMemcpyHostToDevice));
   // (every peer zeroed its pad before contributing its handles to the all-gather above,
   // so no signal can land in an uninitialised pad)
-  p->dev.send = p->win_send;
-  p->p2p_ready = true;
-  if (p->mode == FP8LM_MODE_P2P && N > 1) {
-    int rc = ce_setup(p);
-    if (rc) return rc;
-    if ((rc = qx_setup(p))) return rc;
-  }
-  return FP8LM_OK;
+  return peer_table_upload(p, tab);
 #else
   (void)comm; (void)stream;
   return fail(FP8LM_EUNSUPPORTED, "built without NCCL");
 #endif
+}
+
+int fp8lm_peer_setup_loopback(fp8lm_plan* const* plans, int32_t n, void* stream) {
+  (void)stream;
+  if (!plans || n < 2 || n > FP8LM_MAX_P2P_RANKS)
+    return fail(FP8LM_EINVAL, "peer_setup_loopback: need 2..%d plans", FP8LM_MAX_P2P_RANKS);
+  for (int r = 0; r < n; ++r) {
+    const fp8lm_plan* p = plans[r];
+    if (!p || (p->mode != FP8LM_MODE_P2P && p->mode != FP8LM_MODE_ZERO) || p->mode != plans[0]->mode)
+      return fail(FP8LM_EINVAL, "peer_setup_loopback: plan %d is not P2P / ZERO like plan 0", r);
+    if (!p->bound) return fail(FP8LM_EWORKSPACE, "peer_setup_loopback: plan %d not bound", r);
+    if (p->p2p_ready) return fail(FP8LM_EINVAL, "peer_setup_loopback: plan %d already set up", r);
+    if (p->nranks != n || p->rank != r)
+      return fail(FP8LM_EINVAL, "peer_setup_loopback: plan %d has rank %d of %d", r, p->rank, p->nranks);
+    if (p->numel != plans[0]->numel) return fail(FP8LM_EINVAL, "peer_setup_loopback: plan %d differs", r);
+  }
+  int rc = watchdog_install();
+  if (rc) return rc;
+  CUDA_TRY(preload_kernels());
+  PeerTable tab{};
+  for (int r = 0; r < n; ++r) {
+    if ((rc = peer_alloc(plans[r]))) return rc;
+    tab.send[r] = plans[r]->win_send;
+    tab.g8[r] = plans[r]->win_g8;
+    tab.pad[r] = plans[r]->win_pad;
+    tab.w8[r] = plans[r]->win_w8;
+  }
+  const int ctas = std::max(1, num_sms() / n);
+  for (int r = 0; r < n; ++r) {
+    plans[r]->loopback_ctas = ctas;
+    if (plans[r]->own) plans[r]->own->loopback_ctas = ctas;
+    if ((rc = peer_table_upload(plans[r], tab))) return rc;
+  }
+  return FP8LM_OK;
 }
 
 uint8_t* fp8lm_peer_g8(const fp8lm_plan* p) {
@@ -701,6 +642,7 @@ int fp8lm_sp_create(fp8lm_comm* comm, int64_t max_elems, void* stream, fp8lm_sp*
   tab.pad[rank] = sp->pad;
   if (N > 1) {
 #ifdef FP8LM_WITH_NCCL
+    if (int rc = watchdog_install()) return bail(rc);
     struct Handles { cudaIpcMemHandle_t recv, send, pad; };
     Handles mine;
     if (cudaIpcGetMemHandle(&mine.recv, sp->recv) != cudaSuccess ||
@@ -813,6 +755,7 @@ int fp8lm_allreduce_strategy(int32_t strategy, const float* grads, int32_t nrank
 int fp8lm_amax_scale_sync(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
                           const float* mu, float* amax_out, float* s_g, int32_t* skip,
                           void* stream) {
+  const LaunchScope ls_(p);   // loopback plans: capped grids
   int rc = check_plan(p, comm, "amax_scale_sync");
   if (rc) return rc;
   const void* srcs[FP8LM_MAX_SIM_RANKS];
@@ -852,6 +795,7 @@ int fp8lm_amax_scale_sync(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, in
 int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
                          const float* s_g, const int32_t* skip, uint8_t* g8, float* g_scale,
                          float* g_scale_inv, uint32_t* sat, float* mu, void* stream) {
+  const LaunchScope ls_(p);   // loopback plans: capped grids
   int rc = check_plan(p, comm, "grad_allreduce");
   if (rc) return rc;
   const void* srcs[FP8LM_MAX_SIM_RANKS];
@@ -930,6 +874,7 @@ int fp8lm_adam_step(fp8lm_plan* p, const uint8_t* g8, const float* g_scale_inv,
                     const fp8lm_stensors* m1, const fp8lm_stensors* v,
                     const fp8lm_stensors* master, const fp8lm_stensors* w8,
                     const fp8lm_adam_hp* hp, const int32_t* skip, void* stream) {
+  const LaunchScope ls_(p);   // loopback plans: capped grids
   if (!p) return fail(FP8LM_EINVAL, "adam_step: plan is NULL");
   if (!p->bound) return fail(FP8LM_EWORKSPACE, "adam_step: plan not bound");
   int rc;
@@ -957,6 +902,7 @@ int fp8lm_adam_step_delayed(fp8lm_plan* p, const uint8_t* g8, const float* g_sca
                             const fp8lm_stensors* master, const fp8lm_stensors* w8,
                             const fp8lm_adam_hp* hp, const int32_t* skip, float* w_hist,
                             int32_t hist_slot, void* stream) {
+  const LaunchScope ls_(p);   // loopback plans: capped grids
   if (!p) return fail(FP8LM_EINVAL, "adam_step_delayed: plan is NULL");
   if (!p->bound) return fail(FP8LM_EWORKSPACE, "adam_step_delayed: plan not bound");
   int rc;
@@ -989,6 +935,7 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
                   const fp8lm_stensors* v, const fp8lm_stensors* master,
                   const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
                   int32_t hist_slot, void* stream) {
+  const LaunchScope ls_(p);   // loopback plans: capped grids
   int rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream);
   if (rc) return rc;
   const bool delayed = w_hist != nullptr;
@@ -1046,78 +993,27 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
     if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
     P2PArgs x = p2p_args(p, p->epoch);
-    if (p->ce_chunks > 0) {
-      // copy-engine reduce-scatter: the quantize runs in chunks; after each, a stream
-      // write tells every peer that its part of the chunk is in this send window, and
-      // one copy-engine stream per peer copies the peer's codes of this rank's shard
-      // chunk into recv as soon as the peer's signal arrives — the NVLink transfer runs
-      // under the quantize of the later chunks instead of inside the exchange kernel
-      cudaStream_t s = S(stream);
-      const int N = p->nranks, me = p->rank;
-      const uint32_t eq = ++p->epoch_q;
-      CUDA_TRY(cudaEventRecord(p->ce_events[0], s));     // recv is free after the last step
-      for (int q = 0; q < N; ++q)
-        if (q != me) CUDA_TRY(cudaStreamWaitEvent(p->ce_streams[q], p->ce_events[0], 0));
-      for (int c = 0; c < p->ce_chunks; ++c) {
-        DevPlan dc = p->dev;
-        dc.items = p->ce_items[c];
-        dc.n_items = p->ce_nitems[c];
-        uint8_t* dst[1] = {p->win_send};
-        CUDA_TRY(launch_quantize(dc, srcs, dst, 1, src_dtype, s_g, nullptr, s));
-        for (int q = 0; q < N; ++q) {
-          if (q == me) continue;
-          void* flag = reinterpret_cast<uint8_t*>(p->peer_pad[q]) + kPadFlagQ + 4 * (c * kMaxPeers + me);
-          if (g_write32(s, flag, eq, kWriteFenced) != 0) return fail(FP8LM_ECUDA, "cuStreamWriteValue32 failed");
-        }
-        const int64_t off = c * p->ce_chunk;
-        const int64_t len = std::min(p->ce_chunk, p->shard - off);
-        for (int q = 0; q < N; ++q) {
-          if (q == me) continue;
-          void* flag = reinterpret_cast<uint8_t*>(p->win_pad) + kPadFlagQ + 4 * (c * kMaxPeers + q);
-          if (g_wait32(p->ce_streams[q], flag, eq, kWaitGeq) != 0) return fail(FP8LM_ECUDA, "cuStreamWaitValue32 failed");
-          ProfScope ps_(P_CE_RS, p->ce_streams[q]);
-          CUDA_TRY(cudaMemcpyAsync(p->ce_recv + q * p->shard + off, p->peer_send[q] + me * p->shard + off,
-                                   (size_t)len, cudaMemcpyDeviceToDevice, p->ce_streams[q]));
-        }
-      }
-      for (int q = 0; q < N; ++q) {
-        if (q == me) continue;
-        CUDA_TRY(cudaEventRecord(p->ce_events[1 + q], p->ce_streams[q]));
-        CUDA_TRY(cudaStreamWaitEvent(s, p->ce_events[1 + q], 0));
-      }
-      x.ce_recv = p->ce_recv;
-      x.ce_stride = p->shard;
-      x.ce_lo = p->shard * me;
-    } else if (p->qx.C == 0 || delayed) {   // (k_qx quantizes inside the exchange)
-      uint8_t* dst[1] = {p->win_send};
-      CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
-    }
+    uint8_t* dst[1] = {p->win_send};
+    CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
     // the exchange leaves each rank's reduced shard in its own window; the AdamW pass
     // that encodes the states pulls the other shards' codes from the peers' windows (the
     // all-gather, overlapped with its HBM traffic), walking its work items from this
     // rank's shard on so that the ranks pull from different owners at any moment
-    // (FP8LM_PULL_ROT=0 disables the rotation, diagnosis)
-    static const bool rotate = !getenv("FP8LM_PULL_ROT") || atoi(getenv("FP8LM_PULL_ROT")) != 0;
     const int64_t lo = p->shard * p->rank;
     const auto first = std::lower_bound(p->items.begin(), p->items.end(), lo,
                                         [](const ShardItem& a, int64_t v) { return a.pos < v; });
     Pass2Ext ext;
     ext.pull_tab = x.tab;
     ext.pull_shard = p->shard;
-    ext.rot = rotate ? (int64_t)(first - p->items.begin()) : 0;
+    ext.rot = (int64_t)(first - p->items.begin());
     if (delayed) {            // reduce-scatter only, then the single delayed pass
       CUDA_TRY(launch_reduce_p2p(p->dev, x, g8, s_g, tail, S(stream), /*ag=*/false));
       CUDA_TRY(launch_adam_delayed(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip,
                                    w_hist, hist_slot, S(stream), &ext));
       return FP8LM_OK;
     }
-    if (p->qx.C > 0 && p->ce_chunks == 0) {
-      CUDA_TRY(launch_qx(p->dev, x, s_g, tail, g8, srcs[0], src_dtype, *m1, *v, *master, *w8, *hp,
-                         skip, p->qx, S(stream)));
-    } else {
-      CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip,
-                                    S(stream)));
-    }
+    CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip,
+                                  S(stream)));
     CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream),
                          /*pass1=*/false, &ext));
     return FP8LM_OK;
@@ -1138,6 +1034,7 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
 int fp8lm_state_init(fp8lm_plan* p, const float* w0, const fp8lm_stensors* m1,
                      const fp8lm_stensors* v, const fp8lm_stensors* master,
                      const fp8lm_stensors* w8, void* stream) {
+  const LaunchScope ls_(p);   // loopback plans: capped grids
   if (!p) return fail(FP8LM_EINVAL, "state_init: plan is NULL");
   if (!p->bound) return fail(FP8LM_EWORKSPACE, "state_init: plan not bound");
   int rc;

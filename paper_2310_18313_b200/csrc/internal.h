@@ -55,19 +55,14 @@ constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2, kCtrFix = 3, kCtrFixGen 
 // per-shard saturation counts).
 constexpr int kMaxPeers = FP8LM_MAX_P2P_RANKS;
 constexpr size_t kPadFlagScale = 0, kPadFlagReady = 64, kPadFlagDone = 128, kPadFlagW8 = 192,
-                 kPadTable = 256, kPadFlagQ = 512, kPadData = 1024;
-// copy-engine reduce-scatter (mode P2P dp_step): flag "chunk c of rank r's send window is
-// quantized" at kPadFlagQ + 4 (c kMaxPeers + r), written by rank r's stream
-constexpr int kMaxCeChunks = 16;
+                 kPadTable = 256, kPadData = 1024;
 struct PeerTable {
   uint8_t* send[kMaxPeers];
   uint8_t* g8[kMaxPeers];
   uint32_t* pad[kMaxPeers];
   uint8_t* w8[kMaxPeers];   // mode ZERO: replicated FP8 weight copy (full layout)
 };
-static_assert(kPadTable + sizeof(PeerTable) <= kPadFlagQ &&
-                  kPadFlagQ + 4 * (size_t)kMaxCeChunks * kMaxPeers <= kPadData,
-              "pad layout");
+static_assert(kPadTable + sizeof(PeerTable) <= kPadData, "pad layout");
 // pad data region: scales [N][T] f32 | sat [N][T] u32 | (ZERO) w8 scalars [3][T] f32 |
 // pass-1 state maxima [N][3T] u32 (fused P2P step)
 inline size_t pad_bytes_for(int N, int T) {
@@ -80,12 +75,6 @@ struct P2PArgs {
   int rank;
   int nranks;
   uint32_t epoch;         // step counter: flags hold the epoch of their last signal
-  // copy-engine reduce-scatter: rank r's codes of this rank's shard are already local at
-  // ce_recv + r * ce_stride + (pos - ce_lo) (r != rank; own: the send window), so the
-  // exchange kernel skips its entry barrier.  nullptr: read the peers' send windows.
-  const uint8_t* ce_recv = nullptr;
-  int64_t ce_stride = 0;
-  int64_t ce_lo = 0;
 };
 
 // ---------------------------------------------------------------- FP8 SP converter (f4)
@@ -122,16 +111,6 @@ struct Pass2Ext {
   const int64_t* own_gpos = nullptr;
   const int32_t* own2full = nullptr;
   int T_full = 0;
-};
-
-// quantize + exchange pipeline of the P2P dp_step (k_qx): host view of the chunk tables
-struct QxHost {
-  const ShardItem* qitems = nullptr;   // device
-  const ShardItem* pitems = nullptr;   // device
-  int64_t qoff[kMaxCeChunks + 1] = {};
-  int64_t poff[kMaxCeChunks + 1] = {};
-  int C = 0;
-  uint32_t* ctr = nullptr;             // device [kMaxCeChunks], zero at rest
 };
 
 // outputs of the Eq. 6 / mu tail of fp8lm_grad_allreduce
@@ -174,21 +153,11 @@ struct fp8lm_plan {
   uint32_t epoch_w8 = 0;
   bool p2p_ready = false;
   uint8_t* win_w8 = nullptr;
-  // mode P2P dp_step, copy-engine reduce-scatter: quantize in chunks, each chunk signalled
-  // to the peers by a stream write; one copy-engine stream per peer waits for the peer's
-  // signal and copies the peer's codes of this rank's shard chunk into recv [N][shard]
-  std::vector<uint8_t*> peer_send;
-  std::vector<uint32_t*> peer_pad;
-  int ce_chunks = 0;                 // 0: the exchange kernel pulls over NVLink itself
-  int64_t ce_chunk = 0;              // bytes per chunk of a shard (multiple of 64)
-  uint8_t* ce_recv = nullptr;
-  std::vector<cudaStream_t> ce_streams;
-  std::vector<cudaEvent_t> ce_events; // [0]: step start on the caller's stream; [1 + q]: peer q done
-  std::vector<fp8lm::ShardItem*> ce_items;   // device: per chunk, the clipped quantize items
-  std::vector<int64_t> ce_nitems;
-  uint32_t epoch_q = 0;
-  // quantize + exchange pipeline (k_qx, FP8LM_P2P_QX): chunk tables owned by the plan
-  fp8lm::QxHost qx;
+  // single-process loopback of modes P2P / ZERO (fp8lm_peer_setup_loopback): the N ranks
+  // are N plans of one process on one GPU; every kernel of this plan launches at most
+  // loopback_ctas CTAs (num_sms / N, so the N ranks' kernels are all resident at once:
+  // the spin-waits need that) without the cooperative / PDL attributes.  0: off.
+  int loopback_ctas = 0;
   // mode ZERO: Alg. 1 owners, the owned tensors and the compact sub-plan over them
   std::vector<int32_t> owner, own2full;
   std::vector<int64_t> own_gpos, full2own_off;
@@ -205,8 +174,8 @@ enum ProfId : int {
   P_AMAX = 0, P_SCALE, P_SCALE_FIX, P_QUANTIZE, P_REDUCE, P_AR_FINALIZE, P_ADAM1, P_ADAM2,
   P_ADAM_FINALIZE, P_ADAM_WFIX, P_STATE_INIT, P_Q_SINGLE, P_DQ_SINGLE, P_MEMSET,
   P_NCCL_MIN, P_NCCL_A2A, P_NCCL_AG_SUM, P_REDUCE_P2P, P_QADAM1, P_W8_BCAST, P_ADAM_DELAYED,
-  P_QADAM_DELAYED, P_STRAT_AMAX, P_STRAT_REDUCE, P_SP_ALLGATHER, P_SP_REDUCE_SCATTER, P_CE_RS,
-  P_QX, P_COUNT
+  P_QADAM_DELAYED, P_STRAT_AMAX, P_STRAT_REDUCE, P_SP_ALLGATHER, P_SP_REDUCE_SCATTER,
+  P_COUNT
 };
 bool prof_on();
 struct ProfScope {
@@ -256,10 +225,6 @@ cudaError_t launch_adam_delayed(const DevPlan& p, const uint8_t* g8, const float
                                 const fp8lm_adam_hp& hp, const int32_t* skip, float* w_hist,
                                 int hist_slot, cudaStream_t s, const Pass2Ext* ext = nullptr);
 // mode P2P fused step: exchange + reduce + Adam pass 1 on the own shard (+ maxima exchange)
-cudaError_t launch_qx(const DevPlan& p, const P2PArgs& x, const float* s_g, const TailArgs& tail,
-                      uint8_t* g8, const void* grads, int src_dtype, const fp8lm_stensors& m1,
-                      const fp8lm_stensors& v, const fp8lm_stensors& w, const fp8lm_stensors& w8,
-                      const fp8lm_adam_hp& hp, const int32_t* skip, const QxHost& q, cudaStream_t s);
 cudaError_t launch_reduce_p2p_a1(const DevPlan& p, const P2PArgs& x, const float* s_g,
                                  const TailArgs& tail, uint8_t* g8, const fp8lm_stensors& m1,
                                  const fp8lm_stensors& v, const fp8lm_stensors& w,
@@ -286,4 +251,23 @@ cudaError_t launch_reduce_owner_a1(const DevPlan& p, const DevPlan& o, const P2P
 cudaError_t launch_dq_single(const void* codes, int fmt, int64_t n, const float* scale_inv,
                              float* dst, cudaStream_t s);
 int num_sms();
+
+// Launch policy of the current API call (thread-local, set by LaunchScope in api.cpp):
+// max_ctas > 0 caps every grid (loopback); plain = no cooperative / PDL attributes.
+struct LaunchPolicy {
+  int max_ctas = 0;
+  bool plain = false;
+};
+LaunchPolicy& launch_policy();
+struct LaunchScope {
+  LaunchPolicy saved;
+  explicit LaunchScope(const fp8lm_plan* p);
+  ~LaunchScope() { launch_policy() = saved; }
+};
+
+// the peer-wait watchdog of every compilation unit that spins on peer flags (device.cuh)
+cudaError_t wait_watchdog_set_kernels(unsigned long long ns, uint32_t* report);
+cudaError_t wait_watchdog_set_sp(unsigned long long ns, uint32_t* report);
+// load the code of every kernel a peer-mode step can launch (see kernels.cu)
+cudaError_t preload_kernels();
 }  // namespace fp8lm

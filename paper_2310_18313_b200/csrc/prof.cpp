@@ -16,10 +16,10 @@ static const char* kNames[P_COUNT] = {
     "adam_pass2", "adam_finalize", "adam_wfix", "state_init", "quantize_single", "dequantize_single",
     "memset", "nccl_allreduce_min", "nccl_alltoall", "nccl_allgather+sum", "reduce_p2p", "quantize+adam_pass1", "w8_broadcast", "adam_delayed",
     "quantize+adam_delayed", "strategy_amax", "strategy_reduce",
-    "sp_allgather", "sp_reduce_scatter", "ce_reduce_scatter_copy", "quantize+reduce_p2p"};
+    "sp_allgather", "sp_reduce_scatter"};
 static const bool kIsOurs[P_COUNT] = {true, true, true, true, true, true, true, true, true,
                                       true, true, true, true, false, false, false, false, true,
-                                      true, true, true, true, true, true, true, true, false, true};
+                                      true, true, true, true, true, true, true, true};
 
 struct Rec {
   int id;

@@ -367,13 +367,8 @@ cudaError_t coop_launch(K kernel, int64_t work, cudaStream_t s, Args... args) {
   int per = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kSpT, 0);
   // 2 CTAs per SM: the three grid barriers and their flag polling cost more than the
-  // extra occupancy buys (measured 1, 2, 4, 8 per SM; FP8LM_SP_CTAS_PER_SM overrides)
-  static int cap = -1;
-  if (cap < 0) {
-    const char* e = getenv("FP8LM_SP_CTAS_PER_SM");
-    cap = e ? atoi(e) : 2;
-  }
-  if (cap > 0 && cap < per) per = cap;
+  // extra occupancy buys (measured 1, 2, 4, 8 per SM)
+  if (per > 2) per = 2;
   const int64_t want = (work + kSpT - 1) / kSpT;
   int64_t grid = (int64_t)sms * (per > 0 ? per : 1);
   if (want < grid) grid = want;
@@ -452,5 +447,7 @@ cudaError_t launch_sp_reduce_scatter(const void* dy, int dtype, int64_t m, void*
     default: return cudaErrorInvalidValue;
   }
 }
+
+FP8LM_WAIT_WATCHDOG_HOOK(wait_watchdog_set_sp)
 
 }  // namespace fp8lm

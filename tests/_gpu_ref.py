@@ -59,3 +59,73 @@ def oracle_init(plan, w0_flat, sub=None):
     slices of the device buffer to the host."""
     sub = range(plan.T) if sub is None else sub
     return [OA.init_state(to_np_f32(w0_flat[plan.offsets[t]: plan.offsets[t] + plan.numels[t]])) for t in sub]
+
+
+def compare_rank(B, plan, dp, res, rank, mode, fused, sub=None):
+    """One rank's outputs of one step of modes P2P / ZERO / NCCL vs the N-rank oracle
+    result `res` (of the tensors in `sub`, default all).  Returns a list of mismatch
+    messages (empty = bit-exact).  mode: "p2p" | "zero" | "nccl"."""
+    sub = list(range(plan.T)) if sub is None else list(sub)
+    msgs = []
+    s_g = dp.s_g.cpu().numpy()
+    sat = dp.sat.cpu().numpy()
+    mu = dp.mu.cpu().numpy()
+    gs = dp.g_scale.cpu().numpy()
+    g8 = dp.g8.cpu().numpy()
+    if bool(dp.skip.item()) != res["skip"]:
+        msgs.append(f"rank {rank}: skip differs")
+    own = [tt for tt, _ in dp.layout.entries] if mode == "zero" else None
+    for i, t in enumerate(sub):
+        p = res["per_tensor"][i]
+        sl = slice(plan.offsets[t], plan.offsets[t] + plan.numels[t])
+        if mode == "p2p" and fused:
+            # fused P2P step: the all-gather is pulled inside the AdamW pass, so this rank's
+            # window holds its own shard's codes only (include/fp8lm.h, fp8lm_dp_step)
+            lo = plan.shard_begin(rank)
+            hi = lo + plan.shard_bytes
+            a, b = max(lo, sl.start), min(hi, sl.stop)
+            codes_ok = a >= b or np.array_equal(g8[a:b], p["codes"][a - sl.start:b - sl.start])
+        elif mode == "zero":
+            if plan.owner(t) == rank:                    # ZeRO: only the owner reduces t
+                o = dp.layout.offsets[own.index(t)]
+                codes_ok = np.array_equal(g8[o:o + plan.numels[t]], p["codes"])
+            else:
+                codes_ok = True
+        else:
+            codes_ok = np.array_equal(g8[sl], p["codes"])
+        if p["skip"]:
+            codes_ok = True
+        checks = [("codes", codes_ok), ("s_g", F32(s_g[t]) == p["s_g"]),
+                  ("sat", p["skip"] or int(sat[t]) == p["sat"]), ("scale", F32(gs[t]) == p["scale"]),
+                  ("mu", F32(mu[t]) == res["mu_next"][i])]
+        for name, good in checks:
+            if not good:
+                msgs.append(f"rank {rank} tensor {t}: {name} differs")
+        where = f"rank {rank} tensor {t}"
+        try:
+            ref = res["states"][i]
+            if mode == "zero":
+                w8 = dp.w8_full.cpu().numpy()[sl]
+                sc = dp.w8_full_scalars.cpu().numpy()
+                assert np.array_equal(w8, ref.w8.codes), f"{where}: replicated w8 differs"
+                assert (F32(sc[0, t]), F32(sc[1, t]), F32(sc[2, t])) == \
+                    (ref.w8.scale, ref.w8.scale_inv, ref.w8.amax), f"{where}: replicated w8 scalars differ"
+                if plan.owner(t) == rank:
+                    j = own.index(t)
+                    o, n = dp.layout.offsets[j], plan.numels[t]
+                    st = dp.state
+                    got = dict(
+                        m1=st.m1.data[o:o + n].cpu().numpy(),
+                        v=st.v.data[o:o + n].cpu().view(torch.int16).numpy().view(np.uint16),
+                        master=st.master.data[o:o + n].cpu().view(torch.int16).numpy().view(np.uint16),
+                        w8=st.w8.data[o:o + n].cpu().numpy())
+                    for k in ("m1", "v", "master", "w8"):
+                        s_ = getattr(st, k)
+                        got[k + "_s"] = (F32(s_.scale[j].item()), F32(s_.scale_inv[j].item()),
+                                         F32(s_.amax[j].item()))
+                    assert_state_equal(got, ref, where)
+            else:
+                assert_state_equal(state_np(B, plan, dp.state, t), ref, where)
+        except AssertionError as e:
+            msgs.append(str(e)[:300])
+    return msgs

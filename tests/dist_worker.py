@@ -29,29 +29,6 @@ F32 = np.float32
 NUMELS = [3, 16, 17, 64, 1000, 16384, 16385, 40000, 70001, 5]
 
 
-def check_zero(B, plan, dp, t, ref, where):
-    """Mode ZERO: the owner's compact states of t, and every rank's replicated w8 of t."""
-    w8 = dp.w8_full.cpu().numpy()[plan.offsets[t]: plan.offsets[t] + plan.numels[t]]
-    sc = dp.w8_full_scalars.cpu().numpy()
-    assert np.array_equal(w8, ref.w8.codes), f"{where}: replicated w8 differs"
-    assert (F32(sc[0, t]), F32(sc[1, t]), F32(sc[2, t])) == (ref.w8.scale, ref.w8.scale_inv, ref.w8.amax), \
-        f"{where}: replicated w8 scalars differ"
-    if plan.owner(t) != dist.get_rank():
-        return
-    j = [tt for tt, _ in dp.layout.entries].index(t)
-    o, n = dp.layout.offsets[j], plan.numels[t]
-    st = dp.state
-    got = dict(
-        m1=st.m1.data[o:o + n].cpu().numpy(),
-        v=st.v.data[o:o + n].cpu().view(torch.int16).numpy().view(np.uint16),
-        master=st.master.data[o:o + n].cpu().view(torch.int16).numpy().view(np.uint16),
-        w8=st.w8.data[o:o + n].cpu().numpy())
-    for k in ("m1", "v", "master", "w8"):
-        s_ = getattr(st, k)
-        got[k + "_s"] = (F32(s_.scale[j].item()), F32(s_.scale_inv[j].item()), F32(s_.amax[j].item()))
-    R.assert_state_equal(got, ref, where)
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
@@ -99,51 +76,9 @@ def main():
                             step=step)
         if args.delayed:
             hists = res["hists"]
-        g8 = dp.g8.cpu().numpy() if args.mode != "zero" else None
-        s_g = dp.s_g.cpu().numpy()
-        sat = dp.sat.cpu().numpy()
-        mu = dp.mu.cpu().numpy()
-        gs = dp.g_scale.cpu().numpy()
-        if bool(dp.skip.item()) != res["skip"]:
+        for m in R.compare_rank(B, plan, dp, res, rank, args.mode, not args.unfused):
             ok = False
-            msgs.append(f"step {step}: skip differs")
-        for t in range(plan.T):
-            p = res["per_tensor"][t]
-            sl = slice(plan.offsets[t], plan.offsets[t] + plan.numels[t])
-            if g8 is not None and args.mode == "p2p" and not args.unfused:
-                # fused P2P step: the all-gather is pulled inside pass 2, so this rank's
-                # window holds its own shard's codes only (include/fp8lm.h, fp8lm_dp_step)
-                lo, hi = plan.shard_begin(rank), plan.shard_begin(rank) + plan.shard_bytes
-                a, b = max(lo, sl.start), min(hi, sl.stop)
-                codes_ok = a >= b or np.array_equal(g8[a:b], p["codes"][a - sl.start:b - sl.start])
-            elif g8 is not None:
-                codes_ok = np.array_equal(g8[sl], p["codes"])
-            elif plan.owner(t) == rank:                       # ZeRO: only the owner reduces t
-                j = [tt for tt, _ in dp.layout.entries].index(t)
-                o = dp.layout.offsets[j]
-                codes_ok = np.array_equal(dp.g8.cpu().numpy()[o:o + plan.numels[t]], p["codes"])
-            else:
-                codes_ok = True
-            checks = [
-                ("codes", codes_ok),
-                ("s_g", F32(s_g[t]) == p["s_g"]),
-                ("sat", int(sat[t]) == p["sat"]),
-                ("scale", F32(gs[t]) == p["scale"]),
-                ("mu", F32(mu[t]) == res["mu_next"][t]),
-            ]
-            for name, good in checks:
-                if not good:
-                    ok = False
-                    msgs.append(f"rank {rank} step {step} tensor {t}: {name} differs")
-            try:
-                if args.mode == "zero":
-                    check_zero(B, plan, dp, t, res["states"][t], f"rank {rank} step {step} tensor {t}")
-                else:
-                    R.assert_state_equal(R.state_np(B, plan, dp.state, t), res["states"][t],
-                                         f"rank {rank} step {step} tensor {t}")
-            except AssertionError as e:
-                ok = False
-                msgs.append(str(e)[:300])
+            msgs.append(f"step {step}: {m}")
         mus = res["mu_next"]
         ref_states = res["states"]
     flag = torch.tensor([1 if ok else 0], device="cuda")
