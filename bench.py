@@ -7,14 +7,18 @@ synthetic gradient set already resident in HBM:
   A4/A5 reduce-scatter + FP32 reduce + all-gather, Eq. 6 scale, mu update) ->
   fp8_adam_step (A6 dequant + A7 two-pass JIT FP8 AdamW, FP8 weight copy).
 
-Default workload: BASELINE.json configs[1], "GPT-125M full gradient set (per-layer
-tensors) on 1 B200" (147 tensors, 123.69M params).  --config gpt-7b selects configs[2].
+Default workload: BASELINE.json configs[2], the GPT-7B gradient set (387 tensors, 6.65G
+params, 26.6 GB of fp32 gradient) at N GPUs — the config the metric's "at 1/2/4/8 B200"
+is quoted on.  --config gpt-125m is configs[1] (147 tensors, 123.69M params), c1 is
+configs[0] (one 4096x4096 fp32 gradient, 2 simulated ranks on one GPU), gpt-13b with
+--exchange zero is configs[3], gpt-175b-layer one transformer layer of GPT-175B (12
+tensors, 1.81G params; north_star's "gradient sets shaped like GPT-7B/13B/175B layers").
 N > 1 (torchrun): one rank per GPU, NCCL over NVLink, each rank holding its own full
 gradient set (data parallelism: per-GPU work fixed -> "scaling": "weak").
 
 metric (BASELINE.json): GB/s of algorithmic bytes moved per step, whole job (sum over
 ranks) = N * bytes_per_rank / max-over-ranks step time, where bytes_per_rank = params
-x (27 B at N = 1; 28 + 1/N + 2(N-1)/N B at N >= 2) — SURVEY §8(d).
+x (27 B at N = 1; 28 + 1/N + 2(N-1)/N B at N >= 2; 39 B for c1) — SURVEY §8(d).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -44,13 +48,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="gpt-125m", choices=["gpt-125m", "gpt-7b", "gpt-13b"])
+    ap.add_argument("--config", default="gpt-7b",
+                    choices=["gpt-7b", "gpt-125m", "gpt-13b", "gpt-175b-layer", "c1"])
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"], help="gradient dtype")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl", "zero"],
                     help="N > 1: fused peer-memory reduce-scatter/all-gather kernel (p2p), "
                          "NCCL all-to-all + all-gather around the reduce kernel (nccl), or "
                          "FP8 ZeRO whole-tensor owners over peer memory (zero, config C4)")
-    ap.add_argument("--lr", type=float, default=6e-4)   # GPT-125M max LR, Table 1
+    ap.add_argument("--lr", type=float, default=0.0,
+                    help="0: the paper's max LR of the config (Table 1, P:279-282: 6e-4 for "
+                         "GPT-125M, 3e-4 for 7B, 13B and C1, 6e-5 for 175B)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grad-sets", type=int, default=0,
@@ -64,7 +71,29 @@ def parse():
     return ap.parse_args()
 
 
-def alg_bytes_per_param(N: int, zero: bool = False, delayed: bool = False) -> float:
+CONFIG_INDEX = {"c1": 0, "gpt-125m": 1, "gpt-7b": 2, "gpt-13b": 3, "gpt-175b-layer": None}
+PAPER_LR = {"c1": 3e-4, "gpt-125m": 6e-4, "gpt-7b": 3e-4, "gpt-13b": 3e-4, "gpt-175b-layer": 6e-5}
+C1_RANKS = 2
+WORKLOAD = {
+    "c1": "one 4096x4096 fp32 gradient tensor, 2 simulated ranks on one GPU (BASELINE.json configs[0])",
+    "gpt-125m": "gpt-125m full gradient set (BASELINE.json configs[1])",
+    "gpt-7b": "gpt-7b full gradient set (BASELINE.json configs[2])",
+    "gpt-13b": "gpt-13b full gradient set (BASELINE.json configs[3])",
+    "gpt-175b-layer": "one gpt-175b transformer layer (12 tensors, d = 12288; north_star's 175B layer shapes)",
+}
+
+
+def config_specs(config: str):
+    """Tensor specs of a bench workload."""
+    import synth
+    if config == "c1":
+        return synth.square_set(4096)
+    if config == "gpt-175b-layer":
+        return [s for s in synth.gpt_gradient_set("gpt-175b", 1) if s.name.startswith("layer0.")]
+    return synth.gpt_gradient_set(config)
+
+
+def alg_bytes_per_param(N: int, zero: bool = False, delayed: bool = False, sim: int = 0) -> float:
     """A1 4 + A3 5 + A7 18 at N = 1 (A4/A5 identity); at N >= 2 add the
     reduce (1 + 1/N) and the all-gather write 2(N-1)/N.  ZeRO owner mode (C4): every rank
     reads its gradient twice (A1 4, A3 5), the owner reduce reads N x n/N codes and writes
@@ -72,6 +101,8 @@ def alg_bytes_per_param(N: int, zero: bool = False, delayed: bool = False) -> fl
     writes n (1/N + 1): 11 + 20/N.  Delayed state scaling (R25-R27) runs AdamW in one pass:
     A7 = read g8 1 + m1 1 + v 2 + master 2, write m1 1 + v 2 + master 2 + w8 1 = 12."""
     a7 = 12.0 if delayed else 18.0
+    if sim:       # simulated ranks on one GPU (c1): A1 4N + A3 5N + reduce N + 1 + A7
+        return 10.0 * sim + 1.0 + a7
     if zero:
         return 11.0 + (2.0 + a7) / N
     if N == 1:
@@ -184,93 +215,164 @@ def max_over_ranks(x: float, world: int) -> float:
 
 
 # ------------------------------------------------------------------ oracle (CPU) legs
-def oracle_sample(specs, config):
-    """Bounded sample of the workload for the CPU oracle: the tensors of the first
-    layer(s) (~10-20 s of single-core oracle work for GPT-125M)."""
+# The CPU oracle (oracle/, numpy, one core per process) as it stands, run on every host
+# core: nothing in its arithmetic couples two tensors, so a fixed set of worker processes
+# each owns whole tensors (assigned largest-first to the least-loaded worker) and keeps
+# their optimizer state across steps.  Per step every worker generates its inputs
+# (untimed), meets the others at a barrier, runs oracle.step.train_step on its tensors
+# and reports its start / end time; the step time is the makespan max(end) - min(start).
+def oracle_sample(specs, config, reference=False):
+    """Bounded sample of the workload (tensor indices) for the oracle."""
+    cores = len(os.sched_getaffinity(0))
     if config == "gpt-125m":
-        want = ("layer0.", "layer1.")
-        return [t for t, s in enumerate(specs) if s.name.startswith(want)]
-    # larger models: layer 0's LayerNorms and biases plus its attention projection
-    return [t for t, s in enumerate(specs)
-            if s.name.startswith("layer0.") and (len(s.shape) == 1 or s.name == "layer0.proj.w")]
+        # the whole C2 set (SURVEY §8(d): "timed fully for C1 and C2"); the reference arm,
+        # which runs K + W steps, leaves out the 38.6M embedding (one core, ~20 s)
+        return [t for t, s in enumerate(specs) if not (reference and s.name == "emb.w")]
+    if config == "c1":
+        return [0]
+    # GPT-7B / 13B / 175B layer: the attention projections d x d of the first `cores` layers
+    # (equal tensors: one per core; the smallest matrices of these sets)
+    idx = [t for t, s in enumerate(specs) if s.name.endswith(".proj.w")]
+    return idx[:max(1, min(cores, len(idx)))]
 
 
-def run_oracle_step(specs, idx, rank, step, states, hists=None):
-    """One oracle step; hists (amax(w) rings) selects delayed state scaling.
-    Returns (seconds, states, hists)."""
+def _oracle_worker(conn, barrier, tensors, nranks, delayed, lr):
+    """One oracle process: tensors = [(t, numel)]; conn receives step numbers, None to stop."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
     import numpy as np
     import torch
+    torch.set_num_threads(1)
     import synth
     from oracle import adam as OA
     from oracle import step as OS
-    grads = []
-    for t in idx:
-        g = torch.empty(specs[t].numel, dtype=torch.float32)
-        synth.fill_gradient(g, 1, t, rank)
-        grads.append(g.numpy())
-    t0 = time.perf_counter()
-    res = OS.train_step([grads], [np.float32(1.0)] * len(idx), states, OA.hyper_params(6e-4, step),
-                        hists=hists, step=step)
-    return time.perf_counter() - t0, res["states"], res["hists"]
-
-
-def oracle_states(specs, idx):
-    import torch
-    import synth
-    from oracle import adam as OA
-    out = []
-    for t in idx:
-        w = torch.empty(specs[t].numel, dtype=torch.float32)
+    states = []
+    for t, n in tensors:
+        w = torch.empty(n, dtype=torch.float32)
         synth.fill_weights(w, t)
-        out.append(OA.init_state(w.numpy()))
-    return out
+        states.append(OA.init_state(w.numpy()))
+    hists = [OA.init_history(st) for st in states] if delayed else None
+    mus = [np.float32(1.0)] * len(tensors)
+    conn.send("ready")
+    while True:
+        step = conn.recv()
+        if step is None:
+            break
+        grads = []
+        for r in range(nranks):
+            row = []
+            for t, n in tensors:
+                g = torch.empty(n, dtype=torch.float32)
+                synth.fill_gradient(g, step, t, r)
+                row.append(g.numpy())
+            grads.append(row)
+        barrier.wait()
+        t0 = time.monotonic()
+        res = OS.train_step(grads, mus, states, OA.hyper_params(lr, step), hists=hists, step=step)
+        t1 = time.monotonic()
+        states, mus = res["states"], res["mu_next"]
+        if delayed:
+            hists = res["hists"]
+        conn.send((t0, t1))
 
 
-def oracle_hists(states, delayed):
-    from oracle import adam as OA
-    return [OA.init_history(st) for st in states] if delayed else None
+class OraclePool:
+    """Worker processes (spawn: the parent may hold a CUDA context) over the sample."""
+
+    def __init__(self, specs, idx, nranks=1, delayed=False, lr=3e-4, workers=None):
+        import multiprocessing as mp
+        ctx = mp.get_context("spawn")
+        W = max(1, min(workers or len(os.sched_getaffinity(0)), len(idx)))
+        load = [0] * W
+        parts = [[] for _ in range(W)]
+        for t in sorted(idx, key=lambda t: -specs[t].numel):      # largest first, least loaded
+            j = min(range(W), key=lambda k: load[k])
+            parts[j].append((t, specs[t].numel))
+            load[j] += specs[t].numel
+        self.params = sum(specs[t].numel for t in idx)
+        self.max_part = max(load)
+        self.barrier = ctx.Barrier(W)
+        self.conns, self.procs = [], []
+        for part in parts:
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_oracle_worker, args=(b, self.barrier, part, nranks, delayed, lr),
+                            daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        for c in self.conns:
+            assert c.recv() == "ready"
+        self.workers = W
+        self.step_no = 0
+
+    def step(self):
+        """One oracle step of the whole sample -> (makespan s, per-worker busy s list)."""
+        self.step_no += 1
+        for c in self.conns:
+            c.send(self.step_no)
+        times = [c.recv() for c in self.conns]
+        return max(t[1] for t in times) - min(t[0] for t in times), [t[1] - t[0] for t in times]
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for p in self.procs:
+            p.join(timeout=30)
 
 
-def cpu_baseline(specs, config, delayed=False):
-    idx = oracle_sample(specs, config)
-    params = sum(specs[t].numel for t in idx)
-    states = oracle_states(specs, idx)
-    dt, _, _ = run_oracle_step(specs, idx, 0, 1, states, oracle_hists(states, delayed))
-    gbs = alg_bytes_per_param(1, delayed=delayed) * params / dt / 1e9
-    return {"value": gbs, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{len(idx)} tensors ({params} params: {specs[idx[0]].name}..{specs[idx[-1]].name}) "
-                      f"of {config}, one full step, N=1, numpy single-thread; {dt:.2f} s",
-            "host_cores_available": len(os.sched_getaffinity(0))}
+def _oracle_line(args, specs, pool, secs, busy):
+    nsim = C1_RANKS if args.config == "c1" else 0
+    delayed = args.state_scaling == "delayed"
+    bpp = alg_bytes_per_param(1, delayed=delayed, sim=nsim)
+    value = bpp * pool.params / secs / 1e9
+    # one core: the largest worker's own rate (its params over its busy time)
+    one = bpp * pool.max_part / max(busy) / 1e9
+    total = sum(s.numel for s in specs)
+    cpu = os.popen("grep -m1 'model name' /proc/cpuinfo").read().split(":")[-1].strip()
+    return value, {
+        "value": value, "unit": UNIT, "cores": pool.workers, "kind": "oracle",
+        "sample": (f"{pool.params} of {total} params of {args.config} ({len(specs)} tensors); "
+                   f"whole tensors over {pool.workers} worker processes (one core each), makespan "
+                   f"{secs:.2f} s per step"),
+        "value_1thread": one, "host_cores_available": len(os.sched_getaffinity(0)), "cpu_model": cpu,
+        "extrapolated_full_config_s": total * bpp / (value * 1e9)}
+
+
+def cpu_baseline(args, specs):
+    idx = oracle_sample(specs, args.config)
+    pool = OraclePool(specs, idx, C1_RANKS if args.config == "c1" else 1,
+                      args.state_scaling == "delayed", args.lr)
+    try:
+        secs, busy = pool.step()
+    finally:
+        pool.close()
+    return _oracle_line(args, specs, pool, secs, busy)[1]
 
 
 def run_reference(args, specs, world, rank):
     """--impl reference: the CPU oracle as the reference arm, same metric/config/unit."""
     if rank != 0:
         return
-    idx = oracle_sample(specs, args.config)
-    params = sum(specs[t].numel for t in idx)
-    states = oracle_states(specs, idx)
-    delayed = args.state_scaling == "delayed"
-    hists = oracle_hists(states, delayed)
-    step = 0
-    for _ in range(args.warmup):
-        step += 1
-        _, states, hists = run_oracle_step(specs, idx, 0, step, states, hists)
-    tot = 0.0
-    for _ in range(args.steps):
-        step += 1
-        dt, states, hists = run_oracle_step(specs, idx, 0, step, states, hists)
-        tot += dt
+    idx = oracle_sample(specs, args.config, reference=True)
+    pool = OraclePool(specs, idx, C1_RANKS if args.config == "c1" else 1,
+                      args.state_scaling == "delayed", args.lr)
+    try:
+        for _ in range(args.warmup):
+            pool.step()
+        tot, busy_max = 0.0, []
+        for _ in range(args.steps):
+            secs, busy = pool.step()
+            tot += secs
+            busy_max.append(max(busy))
+    finally:
+        pool.close()
     ms = tot / args.steps * 1e3
-    value = alg_bytes_per_param(1, delayed=delayed) * params / (ms / 1e3) / 1e9
-    sample = (f"{len(idx)} tensors ({params} params) of {args.config} per step, N=1 math, "
-              f"numpy single-thread")
+    value, cpu = _oracle_line(args, specs, pool, ms / 1e3, [statistics.mean(busy_max)])
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config} gradient set, oracle sample", "tensors": len(idx),
-                       "params": params, "state_scaling": args.state_scaling},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+                       "params": pool.params, "state_scaling": args.state_scaling},
+            "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -279,8 +381,9 @@ def run_reference(args, specs, world, rank):
 def main():
     args = parse()
     import synth
-    cfg_layers = None
-    specs = synth.gpt_gradient_set(args.config, cfg_layers)
+    if not args.lr:
+        args.lr = PAPER_LR[args.config]
+    specs = config_specs(args.config)
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))
@@ -294,27 +397,33 @@ def main():
     numels = [s.numel for s in specs]
     params = sum(numels)
     N = world
+    sim = C1_RANKS if args.config == "c1" else 0
+    if sim and N > 1:
+        raise SystemExit("--config c1 is 2 simulated ranks on ONE GPU (BASELINE configs[0])")
     comm = B.Comm.from_torch_distributed() if N > 1 else None
     mode = ({"p2p": B.MODE_P2P, "nccl": B.MODE_NCCL, "zero": B.MODE_ZERO}[args.exchange]
-            if N > 1 else B.MODE_LOCAL)
+            if N > 1 else (B.MODE_SIMULATED if sim else B.MODE_LOCAL))
     zero = mode == B.MODE_ZERO
-    plan = B.Plan(numels, mode=mode, nranks=N, rank=rank)
+    plan = B.Plan(numels, mode=mode, nranks=sim or N, rank=rank)
     gdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     w0 = plan.flat(torch.float32)
     for t, v in enumerate(plan.views(w0)):
         synth.fill_weights(v, t)
-    R = args.grad_sets or {"gpt-125m": 4, "gpt-7b": 2, "gpt-13b": 1}[args.config]
+    R = args.grad_sets or {"gpt-125m": 4, "gpt-7b": 2, "gpt-13b": 1, "gpt-175b-layer": 2, "c1": 4}[args.config]
     # antithetic rotation G1, -G1, G2, -G2, ...: a gradient with a persistent mean drives
     # every weight to the sign-descent fixed point |w| = 1/wd within ~1e3 steps, a state
     # no real run reaches (the weights pile up at amax(w) and crowd the amax screen)
     gsets = []
     for r_ in range(R):
-        g = plan.flat(gdt)
-        for t, v in enumerate(plan.views(g)):
-            synth.fill_gradient(v, 1 + r_ // 2, t, rank)
-        if R % 2 == 0 and r_ % 2 == 1:
-            g.neg_()
-        gsets.append(g)
+        gr = []
+        for rk in (range(sim) if sim else [rank]):
+            g = plan.flat(gdt)
+            for t, v in enumerate(plan.views(g)):
+                synth.fill_gradient(v, 1 + r_ // 2, t, rk)
+            if R % 2 == 0 and r_ % 2 == 1:
+                g.neg_()
+            gr.append(g)
+        gsets.append(gr if sim else gr[0])
     grads = gsets[0]
     delayed = args.state_scaling == "delayed"
     dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr, state_scaling=args.state_scaling)
@@ -377,9 +486,9 @@ def main():
     ms_prof = max_over_ranks(ms_prof_local, world)
     clocks = sampler.stop() if sampler is not None else None
 
-    bytes_rank = alg_bytes_per_param(N, zero, delayed) * params
+    bytes_rank = alg_bytes_per_param(N, zero, delayed, sim) * params
     if args.dtype == "bf16":
-        bytes_rank -= 2.0 * 2 * params      # A1 and A3 read 2 B instead of 4
+        bytes_rank -= 2.0 * 2 * params * max(sim, 1)    # A1 and A3 read 2 B instead of 4
     value = N * bytes_rank / (ms / 1e3) / 1e9
 
     # ---------------- roofline of the dominant kernel (ours, largest device time)
@@ -420,6 +529,8 @@ def main():
     elif dom:
         per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
         bpp = KERNEL_BYTES.get(dom)
+        if sim and dom == "reduce":
+            bpp = sim + 1.0                  # read the N simulated ranks' codes, write the sum
         if bpp is not None:
             if args.dtype == "bf16" and dom in ("amax", "quantize", "quantize+adam_pass1",
                                                 "quantize+adam_delayed"):
@@ -433,13 +544,17 @@ def main():
     if roof is not None:
         # DRAM bytes per launch of the same kernel on the same workload, from the committed
         # `ncu --set full` capture (tools/ncu_traffic.py); null when none was taken
-        try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")))
-            ent = tr[args.config + ("" if N == 1 else f"/n{N}/{args.exchange}")][dom]
+        key = args.config + ("" if N == 1 else f"/n{N}/{args.exchange}") + \
+            ("/delayed" if delayed else "") + ("/bf16" if args.dtype == "bf16" else "")
+        for rnd in ("r2", "r1"):
+            try:
+                tr = json.load(open(os.path.join(ROOT, "profiles", rnd, "ncu_traffic.json")))
+                ent = tr[key][dom]
+            except (OSError, KeyError, ValueError):
+                continue
             roof["traffic"] = ent["dram_bytes_per_launch"]
-            roof["traffic_source"] = "profiles/r1/ncu_traffic.json (" + ent["source"] + ")"
-        except (OSError, KeyError, ValueError):
-            pass
+            roof["traffic_source"] = f"profiles/{rnd}/ncu_traffic.json [{key}] ({ent['source']})"
+            break
     launches = int(sum(v["launches"] for v in ours.values()) / args.steps)
     breakdown = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
                  for k, v in prof.items()}
@@ -455,18 +570,23 @@ def main():
     e2e = None
     if not args.no_e2e and not args.quick:
         host_sets = []
+        dev_bufs = grads if sim else [grads]
+        set_bytes = sum(g.numel() * g.element_size() for g in dev_bufs)
         # large models: one pinned host copy (the H2D cost per step is the same)
-        for g in (gsets if gsets[0].numel() * gsets[0].element_size() < 4e9 else gsets[:1]):
-            h = torch.empty(g.numel(), dtype=gdt, pin_memory=True)
-            h.copy_(g)
-            host_sets.append(h)
-        host_g = host_sets[0]
+        for gs_ in (gsets if set_bytes < 4e9 else gsets[:1]):
+            hs = []
+            for g in (gs_ if sim else [gs_]):
+                h = torch.empty(g.numel(), dtype=gdt, pin_memory=True)
+                h.copy_(g)
+                hs.append(h)
+            host_sets.append(hs)
         out_h = torch.empty(3 * plan.T + 1, dtype=torch.float32, pin_memory=True)
         out_d = torch.empty(3 * plan.T + 1, dtype=torch.float32, device="cuda")
         ne = [0]
 
         def e2e_step():
-            grads.copy_(host_sets[ne[0] % len(host_sets)], non_blocking=True)
+            for d_, h_ in zip(dev_bufs, host_sets[ne[0] % len(host_sets)]):
+                d_.copy_(h_, non_blocking=True)
             ne[0] += 1
             dp.step(grads)
             torch.cat([dp.mu, dp.s_g, dp.sat.float(), dp.skip.float()], out=out_d)
@@ -483,24 +603,22 @@ def main():
         torch.cuda.synchronize()
         ems = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
         e2e = {"value": N * bytes_rank / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
-               "h2d_bytes_per_step": host_g.numel() * host_g.element_size(),
+               "h2d_bytes_per_step": set_bytes,
                "d2h_bytes_per_step": out_h.numel() * 4}
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline and not args.quick:
-        cpu = cpu_baseline(specs, args.config, delayed)
+        cpu = cpu_baseline(args, specs)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": f"{args.config} full gradient set (BASELINE.json configs["
-                                   f"{ {'gpt-125m': 1, 'gpt-7b': 2, 'gpt-13b': 3}[args.config] }])"
-                                   + (", ZeRO owner mode (Alg. 1)" if zero else ""),
+            "config": {"workload": WORKLOAD[args.config] + (", ZeRO owner mode (Alg. 1)" if zero else ""),
                        "tensors": plan.T, "params": params, "grad_dtype": args.dtype,
                        "alg_bytes_per_param_per_rank": bytes_rank / params,
-                       "parallelism": f"dp{N}" if N > 1 else "single", "state_scaling": args.state_scaling,
+                       "parallelism": f"dp{N}" if N > 1 else (f"{sim} simulated ranks" if sim else "single"), "state_scaling": args.state_scaling,
                        "exchange": (args.exchange if N > 1 else "none"),
                        "l2": "inputs larger than L2 (step moves %.2f GB/rank > 126 MB)" % (bytes_rank / 1e9),
                        "grad_sets_rotated": R, "grad_sets_antithetic": R % 2 == 0,
