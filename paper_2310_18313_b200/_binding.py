@@ -16,7 +16,8 @@ from typing import List, Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfp8lm.so")
+# FP8LM_LIB: an experiment build of the same library (A/B timing runs, build.py --out)
+LIB_PATH = os.environ.get("FP8LM_LIB") or os.path.join(_HERE, "libfp8lm.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -55,9 +55,11 @@ def needs_rebuild() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Each source compiles to an object in parallel (kernels.cu dominates), then one link."""
-    if not force and not needs_rebuild():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Each source compiles to an object in parallel (kernels.cu dominates), then one link.
+    out / defines: an experiment build (A/B runs load it through FP8LM_LIB)."""
+    lib_out = out or LIB
+    if not force and out is None and not defines and not needs_rebuild():
         return LIB
     inc, lib = nccl_dirs()
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
@@ -65,7 +67,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
              "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-I", os.path.join(ROOT, "include")]
     if inc:
         flags += ["-DFP8LM_WITH_NCCL", "-I", inc]
-    objdir = os.path.join(HERE, "build")
+    flags += [f"-D{d}" for d in defines]
+    objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(defines).replace("=", ""))
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
@@ -84,15 +87,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc(), *ARCH, "-shared", *objs]
     if lib:
         cmd += ["-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
-    cmd += ["-o", LIB + ".tmp"]
+    cmd += ["-o", lib_out + ".tmp"]
     if verbose:
         print(" ".join(cmd))
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib_out + ".tmp", lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--out", default=None, help="experiment build: output path")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra -D for an experiment build")
+    a = ap.parse_args()
+    print(build(force=a.force or bool(a.out), verbose=True, out=a.out, defines=a.defines))
