@@ -145,3 +145,29 @@ def test_workspace_sizes(B):
     rc, h = _plan(B, numels, B.MODE_NCCL, 4, 1)
     assert B.lib.fp8lm_plan_workspace_bytes(h) >= 2 * B.lib.fp8lm_plan_g8_bytes(h)   # send + recv
     B.lib.fp8lm_plan_destroy(h)
+
+
+def test_sass_paired_fp32_has_no_contracted_products(B):
+    """R16 needs every product of the AdamW sequence rounded on its own.  The paired
+    FP32 bodies (device.cuh P2: FMUL2 / FFMA2) keep additions scalar because ptxas
+    contracts a mul.rn.f32x2 feeding an add.rn.f32x2 into an FFMA2 even under
+    --fmad=false; the only FFMA2 allowed are the 6 per lane pair inside the paired
+    sqrt / division cores (2 + 4), i.e. 48 per 16-element group body, and only in the
+    kernels that contain that body (k_adam<2, .>).  A contracted product would show up
+    as extra FFMA2 here (and as a parity failure on the GPU)."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", B.LIB_PATH], capture_output=True, text=True).stdout
+    counts, fn = {}, None
+    for line in sass.splitlines():
+        if "Function :" in line:
+            fn = line.split("Function :")[1].strip()
+        elif "FFMA2" in line and fn:
+            counts[fn] = counts.get(fn, 0) + 1
+    assert counts, "no FFMA2 at all: the paired pass-2 body is missing"
+    for fn, c in counts.items():
+        assert fn.startswith("_ZN5fp8lm6k_adamILi2E"), (fn, c)
+        assert c == 48, (fn, c)
