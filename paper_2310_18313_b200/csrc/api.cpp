@@ -940,7 +940,11 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
   if (rc) return rc;
   const bool delayed = w_hist != nullptr;
   if (delayed && (hist_slot < 0 || hist_slot >= 16)) return fail(FP8LM_EINVAL, "dp_step: hist_slot not in [0, 16)");
-  if ((p->mode != FP8LM_MODE_LOCAL && p->mode != FP8LM_MODE_P2P && p->mode != FP8LM_MODE_ZERO) ||
+  // SIMULATED with 2..4 ranks (config C1): quantize + rank-order reduce + Adam pass 1 in one
+  // kernel, like LOCAL; more ranks (tests up to 16) and delayed scaling take the three calls
+  const bool sim_fused = p->mode == FP8LM_MODE_SIMULATED && p->nranks <= 4 && !delayed;
+  if ((p->mode != FP8LM_MODE_LOCAL && p->mode != FP8LM_MODE_P2P && p->mode != FP8LM_MODE_ZERO &&
+       !sim_fused) ||
       p->T == 0 || (delayed && p->mode == FP8LM_MODE_ZERO)) {
     rc = fp8lm_grad_allreduce(p, comm, grads, src_dtype, s_g, skip, g8, g_scale, g_scale_inv, sat,
                               mu, stream);
@@ -1018,15 +1022,19 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
                          /*pass1=*/false, &ext));
     return FP8LM_OK;
   }
-  // LOCAL: the codes quantize produces are final, so Adam pass 1 runs in the same kernel
+  // LOCAL: the codes quantize produces are final, so Adam pass 1 runs in the same kernel;
+  // SIMULATED (2..4 ranks): the same kernel quantizes every rank's value and reduces them
   if ((rc = check_stensors(p, m1, "m1", "dp_step")) || (rc = check_stensors(p, v, "v", "dp_step")) ||
       (rc = check_stensors(p, master, "master", "dp_step")) ||
       (rc = check_stensors(p, w8, "w8", "dp_step")))
     return rc;
   if (!hp || !g_scale || !g_scale_inv || !sat) return fail(FP8LM_EINVAL, "dp_step: NULL argument");
   if (!g8 || !aligned(g8, 256)) return fail(FP8LM_EINVAL, "dp_step: g8 NULL or misaligned");
-  const TailArgs tail{1, skip, sat, g_scale, g_scale_inv, mu};
-  CUDA_TRY(launch_adam_fused_local(p->dev, grads, src_dtype, s_g, g8, tail, *m1, *v, *master, *w8,
+  const void* srcs[FP8LM_MAX_SIM_RANKS];
+  int nsrc = 0;
+  if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
+  const TailArgs tail{nsrc, skip, sat, g_scale, g_scale_inv, mu};
+  CUDA_TRY(launch_adam_fused_local(p->dev, srcs, nsrc, src_dtype, s_g, g8, tail, *m1, *v, *master, *w8,
                                    *hp, skip, S(stream), w_hist, hist_slot));
   return FP8LM_OK;
 }

@@ -212,7 +212,9 @@ cudaError_t launch_adam(const DevPlan& p, const uint8_t* g8, const float* g_sinv
                         const fp8lm_stensors& w, const fp8lm_stensors& w8,
                         const fp8lm_adam_hp& hp, const int32_t* skip, cudaStream_t s,
                         bool pass1 = true, const Pass2Ext* ext = nullptr);
-cudaError_t launch_adam_fused_local(const DevPlan& p, const void* grads, int src_dtype,
+// fused quantize (+ the rank-order reduce of nsrc = 2..4 simulated ranks) + Adam pass 1,
+// then pass 2; nsrc = 1: LOCAL (also the delayed single pass when w_hist != nullptr)
+cudaError_t launch_adam_fused_local(const DevPlan& p, const void* const* srcs, int nsrc, int src_dtype,
                                    const float* s_g, uint8_t* g8, const TailArgs& tail,
                                    const fp8lm_stensors& m1, const fp8lm_stensors& v,
                                    const fp8lm_stensors& w, const fp8lm_stensors& w8,
