@@ -531,10 +531,14 @@ def main():
         bpp = KERNEL_BYTES.get(dom)
         if sim and dom == "reduce":
             bpp = sim + 1.0                  # read the N simulated ranks' codes, write the sum
+        if sim and dom == "quantize+adam_pass1":
+            bpp = 4.0 * sim + 6.0            # fused: read N gradients + m1, v, master; write g8
+        if sim and dom == "amax":
+            bpp = 4.0 * sim                  # one launch reads every simulated rank's gradient
         if bpp is not None:
             if args.dtype == "bf16" and dom in ("amax", "quantize", "quantize+adam_pass1",
                                                 "quantize+adam_delayed"):
-                bpp -= 2.0
+                bpp -= 2.0 * (sim if sim and dom != "quantize" else 1)
             np_ = kparams if dom.startswith("adam") else params
             achieved = bpp * np_ / (per_launch_ms / 1e3) / 1e9
             roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",

@@ -278,3 +278,18 @@ def test_amax_screen_fallback_large_lr(B):
 def test_amax_screen_mixed_simulated(B):
     """Moderate lr: some tensors pass the screen, some fall back."""
     _run_and_compare(B, RAGGED, B.MODE_SIMULATED, 2, steps=3, lr=2e-3)
+
+
+@pytest.mark.parametrize("N", [2, 4])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["f32", "bf16"])
+def test_simulated_fused_reduce(B, N, dtype):
+    """fp8lm_dp_step with 2..4 simulated ranks (config C1's path): one kernel quantizes
+    every rank's staged gradient with the shared scale, sums the decoded codes in rank
+    order, requantizes and runs Adam pass 1 — vs the oracle, with a NaN skip step and an
+    overflowing sum (mu halves)."""
+    def specials(flat, r, step):
+        if step == 2 and r == N - 1:
+            flat[70000] = float("nan")
+        if step == 3 and r == 0:
+            flat[1003] = 3.0e5
+    _run_and_compare(B, RAGGED, B.MODE_SIMULATED, N, steps=4, dtype=dtype, specials=specials)
