@@ -55,6 +55,10 @@ def parse():
                     help="N > 1: fused peer-memory reduce-scatter/all-gather kernel (p2p), "
                          "NCCL all-to-all + all-gather around the reduce kernel (nccl), or "
                          "FP8 ZeRO whole-tensor owners over peer memory (zero, config C4)")
+    ap.add_argument("--buckets", type=int, default=1,
+                    help="N > 1, modes p2p / zero: split the tensors into this many buckets (one plan "
+                         "each) and run the step in two phases per bucket (fp8lm_dp_step_split), so "
+                         "the exchange of one bucket overlaps the HBM passes of the others")
     ap.add_argument("--lr", type=float, default=0.0,
                     help="0: the paper's max LR of the config (Table 1, P:279-282: 6e-4 for "
                          "GPT-125M, 3e-4 for 7B, 13B and C1, 6e-5 for 175B)")
@@ -66,6 +70,10 @@ def parse():
     ap.add_argument("--state-scaling", default="jit", choices=["jit", "delayed"],
                     help="optimizer-state scales: just-in-time (two AdamW passes, R19) or "
                          "delayed from a 16-step amax history (one pass, R25-R27)")
+    ap.add_argument("--worst-case", action="store_true",
+                    help="data-dependent worst case: lr 0.05 moves the largest weights far beyond the "
+                         "amax(w') screen's margin, so pass 2's prologue recomputes pass 1 exactly for "
+                         "(nearly) every tensor (DESIGN §5)")
     ap.add_argument("--quick", action="store_true",
                     help="profiling runs (ncu): no clock soak, no e2e, no cpu baseline")
     return ap.parse_args()
@@ -381,6 +389,8 @@ def run_reference(args, specs, world, rank):
 def main():
     args = parse()
     import synth
+    if args.worst_case:
+        args.lr = 0.05
     if not args.lr:
         args.lr = PAPER_LR[args.config]
     specs = config_specs(args.config)
@@ -404,30 +414,44 @@ def main():
     mode = ({"p2p": B.MODE_P2P, "nccl": B.MODE_NCCL, "zero": B.MODE_ZERO}[args.exchange]
             if N > 1 else (B.MODE_SIMULATED if sim else B.MODE_LOCAL))
     zero = mode == B.MODE_ZERO
-    plan = B.Plan(numels, mode=mode, nranks=sim or N, rank=rank)
+    nb = args.buckets if (N > 1 and args.exchange in ("p2p", "zero")) else 1
+    groups = B.bucket_split(numels, nb) if nb > 1 else [list(range(len(numels)))]
+    plans = [B.Plan([numels[t] for t in grp], mode=mode, nranks=sim or N, rank=rank) for grp in groups]
+    plan = plans[0] if nb == 1 else None
     gdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
-    w0 = plan.flat(torch.float32)
-    for t, v in enumerate(plan.views(w0)):
-        synth.fill_weights(v, t)
+    w0s = []
+    for pl, grp in zip(plans, groups):
+        w0 = pl.flat(torch.float32)
+        for j, v in enumerate(pl.views(w0)):
+            synth.fill_weights(v, grp[j])
+        w0s.append(w0)
     R = args.grad_sets or {"gpt-125m": 4, "gpt-7b": 2, "gpt-13b": 1, "gpt-175b-layer": 2, "c1": 4}[args.config]
     # antithetic rotation G1, -G1, G2, -G2, ...: a gradient with a persistent mean drives
     # every weight to the sign-descent fixed point |w| = 1/wd within ~1e3 steps, a state
     # no real run reaches (the weights pile up at amax(w) and crowd the amax screen)
-    gsets = []
+    # gsets[k]: the step input of gradient set k (one flat buffer; a list of the simulated
+    # ranks' buffers; a list of the buckets' buffers); gbufs[k]: its device tensors
+    gsets, gbufs = [], []
     for r_ in range(R):
-        gr = []
-        for rk in (range(sim) if sim else [rank]):
-            g = plan.flat(gdt)
-            for t, v in enumerate(plan.views(g)):
-                synth.fill_gradient(v, 1 + r_ // 2, t, rk)
-            if R % 2 == 0 and r_ % 2 == 1:
-                g.neg_()
-            gr.append(g)
-        gsets.append(gr if sim else gr[0])
+        bufs = []
+        for pl, grp in zip(plans, groups):
+            for rk in (range(sim) if sim else [rank]):
+                g = pl.flat(gdt)
+                for j, v in enumerate(pl.views(g)):
+                    synth.fill_gradient(v, 1 + r_ // 2, grp[j], rk)
+                if R % 2 == 0 and r_ % 2 == 1:
+                    g.neg_()
+                bufs.append(g)
+        gbufs.append(bufs)
+        gsets.append(bufs if (sim or nb > 1) else bufs[0])
     grads = gsets[0]
     delayed = args.state_scaling == "delayed"
-    dp = B.FP8DataParallel(plan, w0, comm=comm, lr=args.lr, state_scaling=args.state_scaling)
-    del w0
+    if nb > 1:
+        dp = B.BucketedDP(plans, w0s, comm=comm, lr=args.lr, state_scaling=args.state_scaling)
+    else:
+        dp = B.FP8DataParallel(plans[0], w0s[0], comm=comm, lr=args.lr, state_scaling=args.state_scaling)
+    dps = dp.dps if nb > 1 else [dp]
+    del w0s
     torch.cuda.synchronize()
     nstep = [0]
 
@@ -496,15 +520,18 @@ def main():
     ours = {k: v for k, v in prof.items() if v["ours"]}
     dom = max(ours, key=lambda k: ours[k]["ms"]) if ours else None
     roof = None
-    kparams = sum(dp.layout.numels) if zero else params     # AdamW runs on owned tensors only
+    kparams = sum(sum(d.layout.numels) for d in dps) if zero else params   # AdamW: owned tensors only
+    # launches per step of the dominant kernel (buckets: one per bucket): bytes per launch
+    # are the per-step bytes over that count
+    lps = max(1.0, ours[dom]["launches"] / args.steps) if dom else 1.0
     if zero and dom == "adam_pass2" and N > 1:
         # ZeRO dp_step: the owner's pass 2 also stores every w8 code into the N-1 peers'
         # windows, (N-1) bytes per owned parameter out of this GPU over NVLink, under its
         # own 12 B/param of HBM traffic; the link is the bound (the HBM fraction rides along)
         per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
-        nvb = (N - 1) * kparams
+        nvb = (N - 1) * kparams / lps
         achieved = nvb / (per_launch_ms / 1e3) / 1e9
-        hbm_ach = KERNEL_BYTES["adam_pass2"] * kparams / (per_launch_ms / 1e3) / 1e9
+        hbm_ach = KERNEL_BYTES["adam_pass2"] * kparams / lps / (per_launch_ms / 1e3) / 1e9
         roof = {"bound": "nvlink", "kernel": dom, "achieved": achieved, "peak": NVLINK_PEER_GBS,
                 "unit": "GB/s", "frac": achieved / NVLINK_PEER_GBS,
                 "peak_kind": "measured peer copy per direction (B200_PROFILING.md); 900 nominal",
@@ -518,7 +545,7 @@ def main():
         # inside the AdamW pass that encodes the states, so the exchange kernel moves
         # only those; the ZeRO owner reduce pulls (N-1)/N as well.
         per_launch_ms = ours[dom]["ms"] / ours[dom]["launches"]
-        nvb = 1.0 * (N - 1) / N * params
+        nvb = 1.0 * (N - 1) / N * params / lps
         achieved = nvb / (per_launch_ms / 1e3) / 1e9
         roof = {"bound": "nvlink", "kernel": dom, "achieved": achieved, "peak": NVLINK_PEER_GBS,
                 "unit": "GB/s", "frac": achieved / NVLINK_PEER_GBS,
@@ -539,7 +566,7 @@ def main():
             if args.dtype == "bf16" and dom in ("amax", "quantize", "quantize+adam_pass1",
                                                 "quantize+adam_delayed"):
                 bpp -= 2.0 * (sim if sim and dom != "quantize" else 1)
-            np_ = kparams if dom.startswith("adam") else params
+            np_ = (kparams if dom.startswith("adam") else params) / lps
             achieved = bpp * np_ / (per_launch_ms / 1e3) / 1e9
             roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "peak_kind": hbm_kind, "traffic": None,
@@ -574,18 +601,19 @@ def main():
     e2e = None
     if not args.no_e2e and not args.quick:
         host_sets = []
-        dev_bufs = grads if sim else [grads]
+        dev_bufs = gbufs[0]
         set_bytes = sum(g.numel() * g.element_size() for g in dev_bufs)
         # large models: one pinned host copy (the H2D cost per step is the same)
-        for gs_ in (gsets if set_bytes < 4e9 else gsets[:1]):
+        for bufs in (gbufs if set_bytes < 4e9 else gbufs[:1]):
             hs = []
-            for g in (gs_ if sim else [gs_]):
+            for g in bufs:
                 h = torch.empty(g.numel(), dtype=gdt, pin_memory=True)
                 h.copy_(g)
                 hs.append(h)
             host_sets.append(hs)
-        out_h = torch.empty(3 * plan.T + 1, dtype=torch.float32, pin_memory=True)
-        out_d = torch.empty(3 * plan.T + 1, dtype=torch.float32, device="cuda")
+        nres = sum(3 * d.plan.T + 1 for d in dps)
+        out_h = torch.empty(nres, dtype=torch.float32, pin_memory=True)
+        out_d = torch.empty(nres, dtype=torch.float32, device="cuda")
         ne = [0]
 
         def e2e_step():
@@ -593,7 +621,8 @@ def main():
                 d_.copy_(h_, non_blocking=True)
             ne[0] += 1
             dp.step(grads)
-            torch.cat([dp.mu, dp.s_g, dp.sat.float(), dp.skip.float()], out=out_d)
+            torch.cat([x for d in dps for x in (d.mu[:d.plan.T], d.s_g[:d.plan.T], d.sat[:d.plan.T].float(),
+                                                d.skip.float())], out=out_d)
             out_h.copy_(out_d, non_blocking=True)
         for _ in range(2):
             e2e_step()
@@ -620,7 +649,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": WORKLOAD[args.config] + (", ZeRO owner mode (Alg. 1)" if zero else ""),
-                       "tensors": plan.T, "params": params, "grad_dtype": args.dtype,
+                       "tensors": len(numels), "params": params, "grad_dtype": args.dtype,
+                       "buckets": nb, "lr": args.lr,
+                       "case": "worst (amax(w') screen fallback)" if args.worst_case else "typical",
                        "alg_bytes_per_param_per_rank": bytes_rank / params,
                        "parallelism": f"dp{N}" if N > 1 else (f"{sim} simulated ranks" if sim else "single"), "state_scaling": args.state_scaling,
                        "exchange": (args.exchange if N > 1 else "none"),

@@ -313,6 +313,25 @@ int fp8lm_dp_step(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t
                   const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
                   int32_t hist_slot, void* stream);
 
+/* The P2P / ZERO step in two phases, so that the exchange of one bucket of tensors runs
+ * beside the HBM passes of another (the exchange overlaps compute; f2).  A bucket
+ * is a plan over a subset of the tensors (its own windows, flags and epochs).  phase 1:
+ * amax + scale MIN + quantize on `stream`, then the exchange kernel (reduce-scatter +
+ * rank-order reduce + Adam pass 1 on the own shard; ZERO: the owner reduce + pass 1) on
+ * the plan's own high-priority exchange stream; phase 2: `stream` waits for that
+ * exchange, then the AdamW pass with the pulled all-gather (ZERO: + w8 broadcast).  A
+ * caller with buckets b = 0..B-1 issues phase 1 for every bucket, then phase 2 for every
+ * bucket: the exchange of bucket b overlaps the amax / quantize of b+1 and pass 2 of b-1.
+ * Same arguments and results as fp8lm_dp_step (comm unused: modes P2P / ZERO only; ZERO
+ * JIT only).  EINVAL on another mode or when phases do not alternate 1, 2, 1, 2, ...
+ * Every rank must issue the same sequence (the phases are collective). */
+int fp8lm_dp_step_split(fp8lm_plan* plan, int32_t phase, const void* grads, int32_t src_dtype,
+                        float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                        float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
+                        const fp8lm_stensors* v, const fp8lm_stensors* master,
+                        const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
+                        int32_t hist_slot, void* stream);
+
 /* Initial optimizer state: m1, v = zero codes with scale 1,
  * amax 0; master / w8 JIT-encoded from the FP32 flat weights w0 (plan layout).
  * Mode ZERO: w0 and the states are COMPACT (owned tensors); the replicated w8 copy is

@@ -12,5 +12,5 @@ from ._binding import (  # noqa: F401
     amax_scale_sync, fp8_adam_step, fp8_adam_step_delayed, fp8_dequantize, fp8_grad_allreduce, fp8_quantize,
     has_nccl, lib, LIB_PATH, prof_enable, prof_read, state_init, version, zero_plan,
     STRATEGIES, allreduce_strategy, commstats_buffer, commstats_read, SPConverter,
-    peer_setup_loopback, peer_timeout_report, set_peer_timeout,
+    peer_setup_loopback, peer_timeout_report, set_peer_timeout, BucketedDP, bucket_split,
 )

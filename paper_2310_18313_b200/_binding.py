@@ -95,6 +95,9 @@ _sig("fp8lm_selftest_fastmath", C.c_int, _u64, _u64, C.POINTER(_u64))
 _sig("fp8lm_dp_step", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
      C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(AdamHP), _p, _i32, _p)
+_sig("fp8lm_dp_step_split", C.c_int, _p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
+     C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors),
+     C.POINTER(AdamHP), _p, _i32, _p)
 _sig("fp8lm_adam_step_delayed", C.c_int, _p, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(STensors), C.POINTER(STensors), C.POINTER(AdamHP), _p, _p, _i32, _p)
 _sig("fp8lm_sp_create", C.c_int, _p, _i64, _p, C.POINTER(_p))
@@ -631,6 +634,32 @@ class FP8DataParallel:
                                      _stream(stream)), "fp8lm_dp_step")
             del keep
             return
+        self._three_calls(grads, hp, stream)
+
+    def _split(self, phase: int, grads, hp: AdamHP, stream):
+        g, dt, keep = _grads_arg(self.plan, grads) if grads is not None else (None, F32, None)
+        st = self.state
+        m1, v, w, w8 = st.m1.c(), st.v.c(), st.master.c(), st.w8.c()
+        _check(lib.fp8lm_dp_step_split(self.plan.handle, phase, g, dt, _ptr(self.mu), _ptr(self.amax),
+                                       _ptr(self.s_g), _ptr(self.skip), _ptr(self.g8), _ptr(self.g_scale),
+                                       _ptr(self.g_scale_inv), _ptr(self.sat), C.byref(m1), C.byref(v),
+                                       C.byref(w), C.byref(w8), C.byref(hp), _ptr(self.w_hist),
+                                       (self.t - 1) % 16, _stream(stream)), "fp8lm_dp_step_split")
+        del keep
+
+    def step_begin(self, grads, lr: float = None, stream=None):
+        """Phase 1 of fp8lm_dp_step_split (modes P2P / ZERO): amax, scale MIN and quantize on
+        the stream, the exchange on the plan's exchange stream."""
+        self.t += 1
+        self._hp = adam_hp(self.lr if lr is None else lr, self.t, self.betas[0], self.betas[1], self.eps,
+                           self.wd)
+        self._split(1, grads, self._hp, stream)
+
+    def step_end(self, stream=None):
+        """Phase 2: wait for this plan's exchange, then the AdamW pass (pulled all-gather)."""
+        self._split(2, None, self._hp, stream)
+
+    def _three_calls(self, grads, hp, stream):
         amax_scale_sync(self.plan, grads, self.mu, self.amax, self.s_g, self.skip, self.comm, stream)
         fp8_grad_allreduce(self.plan, grads, self.s_g, self.skip, self.g8, self.g_scale,
                            self.g_scale_inv, self.sat, self.mu, self.comm, stream)
@@ -639,3 +668,36 @@ class FP8DataParallel:
                                   self.w_hist, (self.t - 1) % 16, stream)
         else:
             fp8_adam_step(self.plan, self.g8, self.g_scale_inv, self.state, hp, self.skip, stream)
+
+
+# ------------------------------------------------------------------ bucketed step (f2)
+def bucket_split(numels: Sequence[int], buckets: int) -> List[List[int]]:
+    """Contiguous groups of tensor indices with about equal parameter counts."""
+    total = sum(numels)
+    out, cur, acc = [], [], 0
+    for t, n in enumerate(numels):
+        cur.append(t)
+        acc += n
+        if len(out) < buckets - 1 and acc >= total * (len(out) + 1) / buckets:
+            out.append(cur)
+            cur = []
+    if cur:
+        out.append(cur)
+    return out
+
+
+class BucketedDP:
+    """Modes P2P / ZERO with the tensors split into buckets (one plan each): every step
+    issues phase 1 of every bucket, then phase 2 of every bucket (fp8lm_dp_step_split),
+    so the exchange of bucket b runs on its exchange stream beside the amax / quantize of
+    bucket b+1 and the AdamW pass of bucket b-1 on the caller's stream."""
+
+    def __init__(self, plans: Sequence[Plan], w0s: Sequence[torch.Tensor], comm: Comm = None, **kw):
+        self.plans = list(plans)
+        self.dps = [FP8DataParallel(p, w, comm=comm, **kw) for p, w in zip(self.plans, w0s)]
+
+    def step(self, grads: Sequence[torch.Tensor], lr: float = None, stream=None):
+        for dp, g in zip(self.dps, grads):
+            dp.step_begin(g, lr, stream)
+        for dp in self.dps:
+            dp.step_end(stream)

@@ -283,6 +283,9 @@ int fp8lm_plan_destroy(fp8lm_plan* plan) {
   if (plan->win_g8) cudaFree(plan->win_g8);
   if (plan->win_pad) cudaFree(plan->win_pad);
   if (plan->win_w8) cudaFree(plan->win_w8);
+  if (plan->xs) cudaStreamDestroy(plan->xs);
+  if (plan->ev_q) cudaEventDestroy(plan->ev_q);
+  if (plan->ev_x) cudaEventDestroy(plan->ev_x);
   if (plan->own) fp8lm_plan_destroy(plan->own);
   delete plan;
   return FP8LM_OK;
@@ -439,7 +442,9 @@ int fp8lm_peer_setup_loopback(fp8lm_plan* const* plans, int32_t n, void* stream)
     tab.pad[r] = plans[r]->win_pad;
     tab.w8[r] = plans[r]->win_w8;
   }
-  const int ctas = std::max(1, num_sms() / n);
+  // half the SMs per rank's kernel: with the split step two kernels of a rank (its stream
+  // and its exchange stream) can be in flight
+  const int ctas = std::max(1, num_sms() / (2 * n));
   for (int r = 0; r < n; ++r) {
     plans[r]->loopback_ctas = ctas;
     if (plans[r]->own) plans[r]->own->loopback_ctas = ctas;
@@ -929,15 +934,31 @@ int fp8lm_adam_step_delayed(fp8lm_plan* p, const uint8_t* g8, const float* g_sca
 }
 
 // ---------------------------------------------------------------- the whole step
-int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
-                  float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
-                  float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
-                  const fp8lm_stensors* v, const fp8lm_stensors* master,
-                  const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
-                  int32_t hist_slot, void* stream) {
+// the exchange stream of a split step (phase 1 launches the exchange kernel there, phase 2
+// makes the caller's stream wait for it): created on first use, highest priority so its
+// CTAs are scheduled ahead of the HBM passes they run beside
+static int split_resources(fp8lm_plan* p) {
+  if (p->xs) return FP8LM_OK;
+  int lo = 0, hi = 0;
+  CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CUDA_TRY(cudaStreamCreateWithPriority(&p->xs, cudaStreamNonBlocking, hi));
+  CUDA_TRY(cudaEventCreateWithFlags(&p->ev_q, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&p->ev_x, cudaEventDisableTiming));
+  return FP8LM_OK;
+}
+
+// phase 0: the whole step on `stream`; 1: amax + quantize on `stream`, the exchange kernel
+// on the plan's exchange stream; 2: `stream` waits for that exchange, then the AdamW pass
+static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
+                        float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                        float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
+                        const fp8lm_stensors* v, const fp8lm_stensors* master,
+                        const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
+                        int32_t hist_slot, void* stream, int phase) {
   const LaunchScope ls_(p);   // loopback plans: capped grids
-  int rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream);
-  if (rc) return rc;
+  int rc;
+  if (phase != 2 && (rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream)))
+    return rc;
   const bool delayed = w_hist != nullptr;
   if (delayed && (hist_slot < 0 || hist_slot >= 16)) return fail(FP8LM_EINVAL, "dp_step: hist_slot not in [0, 16)");
   // SIMULATED with 2..4 ranks (config C1): quantize + rank-order reduce + Adam pass 1 in one
@@ -960,14 +981,28 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
     if (!hp || !g_scale || !g_scale_inv || !sat || !m1 || !v || !master || !w8)
       return fail(FP8LM_EINVAL, "dp_step: NULL argument");
     if (p->own->T > 0 && (!g8 || !aligned(g8, 256))) return fail(FP8LM_EINVAL, "dp_step: g8 NULL or misaligned");
-    const void* srcs[1];
-    int nsrc = 0;
-    if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
-    uint8_t* dst[1] = {p->win_send};
-    CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
-    CUDA_TRY(launch_reduce_owner_a1(p->dev, p->own->dev, p2p_args(p, p->epoch), s_g, tail, g8, *m1, *v,
-                                    *master, *w8, *hp, skip, S(stream)));
+    if (phase != 2) {
+      const void* srcs[1];
+      int nsrc = 0;
+      if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
+      uint8_t* dst[1] = {p->win_send};
+      CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
+      cudaStream_t xs = S(stream);
+      if (phase == 1) {
+        CUDA_TRY(cudaEventRecord(p->ev_q, S(stream)));
+        CUDA_TRY(cudaStreamWaitEvent(p->xs, p->ev_q, 0));
+        xs = p->xs;
+      }
+      CUDA_TRY(launch_reduce_owner_a1(p->dev, p->own->dev, p2p_args(p, p->epoch), s_g, tail, g8, *m1, *v,
+                                      *master, *w8, *hp, skip, xs));
+      if (phase == 1) {
+        CUDA_TRY(cudaEventRecord(p->ev_x, p->xs));
+        return FP8LM_OK;
+      }
+    } else {
+      CUDA_TRY(cudaStreamWaitEvent(S(stream), p->ev_x, 0));
+    }
     // pass 2 on the owned tensors also stores every w8 group into every rank's window
     // (the broadcast overlaps the HBM-bound pass); its last CTA publishes the scalars
     Pass2Ext ext;
@@ -992,13 +1027,31 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
       return rc;
     if (!hp || !g_scale || !g_scale_inv || !sat) return fail(FP8LM_EINVAL, "dp_step: NULL argument");
     if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "dp_step: mode P2P needs g8 == fp8lm_peer_g8(plan)");
-    const void* srcs[1];
-    int nsrc = 0;
-    if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
     P2PArgs x = p2p_args(p, p->epoch);
-    uint8_t* dst[1] = {p->win_send};
-    CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
+    if (phase != 2) {
+      const void* srcs[1];
+      int nsrc = 0;
+      if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
+      uint8_t* dst[1] = {p->win_send};
+      CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
+      cudaStream_t xs = S(stream);
+      if (phase == 1) {
+        CUDA_TRY(cudaEventRecord(p->ev_q, S(stream)));
+        CUDA_TRY(cudaStreamWaitEvent(p->xs, p->ev_q, 0));
+        xs = p->xs;
+      }
+      if (delayed)            // reduce-scatter only (the single delayed pass pulls the rest)
+        CUDA_TRY(launch_reduce_p2p(p->dev, x, g8, s_g, tail, xs, /*ag=*/false));
+      else
+        CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip, xs));
+      if (phase == 1) {
+        CUDA_TRY(cudaEventRecord(p->ev_x, p->xs));
+        return FP8LM_OK;
+      }
+    } else {
+      CUDA_TRY(cudaStreamWaitEvent(S(stream), p->ev_x, 0));
+    }
     // the exchange leaves each rank's reduced shard in its own window; the AdamW pass
     // that encodes the states pulls the other shards' codes from the peers' windows (the
     // all-gather, overlapped with its HBM traffic), walking its work items from this
@@ -1010,18 +1063,16 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
     ext.pull_tab = x.tab;
     ext.pull_shard = p->shard;
     ext.rot = (int64_t)(first - p->items.begin());
-    if (delayed) {            // reduce-scatter only, then the single delayed pass
-      CUDA_TRY(launch_reduce_p2p(p->dev, x, g8, s_g, tail, S(stream), /*ag=*/false));
+    if (delayed) {            // the single delayed pass
       CUDA_TRY(launch_adam_delayed(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip,
                                    w_hist, hist_slot, S(stream), &ext));
       return FP8LM_OK;
     }
-    CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip,
-                                  S(stream)));
     CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream),
                          /*pass1=*/false, &ext));
     return FP8LM_OK;
   }
+  if (phase != 0) return fail(FP8LM_EINVAL, "dp_step_split: modes P2P / ZERO only");
   // LOCAL: the codes quantize produces are final, so Adam pass 1 runs in the same kernel;
   // SIMULATED (2..4 ranks): the same kernel quantizes every rank's value and reduces them
   if ((rc = check_stensors(p, m1, "m1", "dp_step")) || (rc = check_stensors(p, v, "v", "dp_step")) ||
@@ -1037,6 +1088,37 @@ int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t sr
   CUDA_TRY(launch_adam_fused_local(p->dev, srcs, nsrc, src_dtype, s_g, g8, tail, *m1, *v, *master, *w8,
                                    *hp, skip, S(stream), w_hist, hist_slot));
   return FP8LM_OK;
+}
+
+int fp8lm_dp_step(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
+                  float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                  float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
+                  const fp8lm_stensors* v, const fp8lm_stensors* master,
+                  const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
+                  int32_t hist_slot, void* stream) {
+  return dp_step_impl(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, g8, g_scale, g_scale_inv, sat,
+                      m1, v, master, w8, hp, w_hist, hist_slot, stream, 0);
+}
+
+int fp8lm_dp_step_split(fp8lm_plan* p, int32_t phase, const void* grads, int32_t src_dtype,
+                        float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                        float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
+                        const fp8lm_stensors* v, const fp8lm_stensors* master,
+                        const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
+                        int32_t hist_slot, void* stream) {
+  if (!p || (p->mode != FP8LM_MODE_P2P && p->mode != FP8LM_MODE_ZERO))
+    return fail(FP8LM_EINVAL, "dp_step_split: modes P2P / ZERO only");
+  if (phase != 1 && phase != 2) return fail(FP8LM_EINVAL, "dp_step_split: phase must be 1 or 2");
+  if (w_hist && p->mode == FP8LM_MODE_ZERO)
+    return fail(FP8LM_EINVAL, "dp_step_split: mode ZERO with delayed state scaling has no split form");
+  if ((phase == 2) != p->split_open)
+    return fail(FP8LM_EINVAL, "dp_step_split: phase %d out of order (phases 1 and 2 alternate)", phase);
+  int rc = split_resources(p);
+  if (rc) return rc;
+  rc = dp_step_impl(p, nullptr, grads, src_dtype, mu, amax_out, s_g, skip, g8, g_scale, g_scale_inv, sat,
+                    m1, v, master, w8, hp, w_hist, hist_slot, stream, phase);
+  if (!rc) p->split_open = phase == 1;
+  return rc;
 }
 
 int fp8lm_state_init(fp8lm_plan* p, const float* w0, const fp8lm_stensors* m1,

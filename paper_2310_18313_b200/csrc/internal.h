@@ -158,6 +158,10 @@ struct fp8lm_plan {
   // loopback_ctas CTAs (num_sms / N, so the N ranks' kernels are all resident at once:
   // the spin-waits need that) without the cooperative / PDL attributes.  0: off.
   int loopback_ctas = 0;
+  // split step (fp8lm_dp_step_split): the exchange stream and its two events
+  cudaStream_t xs = nullptr;
+  cudaEvent_t ev_q = nullptr, ev_x = nullptr;
+  bool split_open = false;
   // mode ZERO: Alg. 1 owners, the owned tensors and the compact sub-plan over them
   std::vector<int32_t> owner, own2full;
   std::vector<int64_t> own_gpos, full2own_off;

@@ -4,6 +4,11 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# the loopback tests run up to 2 kernels per logical rank concurrently (its stream and its
+# exchange stream) whose CTAs meet at peer flags: with the default 8 hardware work queues
+# two of those streams can share a queue, serialising a waiting kernel in front of the one
+# it waits for.  32 queues (the maximum) give every stream its own (set before CUDA init).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

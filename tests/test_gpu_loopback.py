@@ -138,3 +138,72 @@ def test_loopback_gpt125m_sampled(B, mode, N):
     big = [t for t in straddle if numels[t] > 8_000_000]
     sub = sorted(set([t for t in straddle if t not in big][:3] + [1, 2, 3, 9, len(specs) - 2, len(specs) - 1]))
     run_loopback(B, numels, mode, N, steps=2, sub=sub)
+
+
+@pytest.mark.parametrize("N", [2, 4])
+@pytest.mark.parametrize("variant", ["p2p", "p2p_delayed", "zero"])
+def test_loopback_split_buckets(B, N, variant):
+    """fp8lm_dp_step_split over 3 buckets (one plan each): phase 1 of every bucket (amax,
+    MIN, quantize; the exchange on the plan's exchange stream), then phase 2 of every
+    bucket (the AdamW pass with the pulled all-gather / the w8 broadcast).  Each bucket
+    is an independent scaling group (R33), checked against the oracle on its tensors."""
+    import synth
+    mode = variant.split("_")[0]
+    delayed = "delayed" in variant
+    bmode = {"p2p": B.MODE_P2P, "zero": B.MODE_ZERO}[mode]
+    groups = B.bucket_split(RAGGED, 3)
+    assert len(groups) == 3
+    plans = [[B.Plan([RAGGED[t] for t in grp], mode=bmode, nranks=N, rank=r) for grp in groups]
+             for r in range(N)]
+    for b in range(len(groups)):
+        B.peer_setup_loopback([plans[r][b] for r in range(N)])
+    streams = [torch.cuda.Stream() for _ in range(N)]
+    w0s = []
+    for b, grp in enumerate(groups):
+        w = plans[0][b].flat(torch.float32)
+        for j, v in enumerate(plans[0][b].views(w)):
+            synth.fill_weights(v, grp[j])
+        w0s.append(w)
+    torch.cuda.synchronize()
+    dps = []
+    for r in range(N):
+        with torch.cuda.stream(streams[r]):
+            dps.append(B.BucketedDP(plans[r], w0s, state_scaling="delayed" if delayed else "jit"))
+    torch.cuda.synchronize()
+    refs = [R.oracle_init(plans[0][b], w0s[b]) for b in range(len(groups))]
+    mus = [[F32(1.0)] * len(g) for g in groups]
+    hists = [[OA.init_history(st) for st in rs] for rs in refs] if delayed else None
+    for step in range(1, 4):
+        grads = []
+        for r in range(N):
+            row = []
+            for b, grp in enumerate(groups):
+                flat = plans[0][b].flat(torch.float32)
+                for j, v in enumerate(plans[0][b].views(flat)):
+                    synth.fill_gradient(v, step, grp[j], r)
+                if step == 2 and r == N - 1 and b == 1:
+                    flat[plans[0][b].offsets[0] + 3] = 3.0e5      # bucket 1's sum saturates
+                row.append(flat)
+            grads.append(row)
+        torch.cuda.synchronize()
+        try:
+            for r in range(N):
+                with torch.cuda.stream(streams[r]):
+                    dps[r].step(grads[r])
+            torch.cuda.synchronize()
+        except Exception as e:
+            raise AssertionError(f"step {step}: {e}; watchdog report {B.peer_timeout_report()}") from e
+        msgs = []
+        for b, grp in enumerate(groups):
+            plan = plans[0][b]
+            per_rank = [[R.to_np_f32(grads[r][b][plan.offsets[j]: plan.offsets[j] + plan.numels[j]])
+                         for j in range(plan.T)] for r in range(N)]
+            res = OS.train_step(per_rank, mus[b], refs[b], OA.hyper_params(3e-4, step),
+                                hists=hists[b] if delayed else None, step=step)
+            for r in range(N):
+                msgs += [f"step {step} bucket {b}: {m}" for m in
+                         R.compare_rank(B, plans[r][b], dps[r].dps[b], res, r, mode, True)]
+            mus[b], refs[b] = res["mu_next"], res["states"]
+            if delayed:
+                hists[b] = res["hists"]
+        assert not msgs, "\n".join(msgs[:10])

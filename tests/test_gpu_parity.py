@@ -293,3 +293,80 @@ def test_simulated_fused_reduce(B, N, dtype):
         if step == 3 and r == 0:
             flat[1003] = 3.0e5
     _run_and_compare(B, RAGGED, B.MODE_SIMULATED, N, steps=4, dtype=dtype, specials=specials)
+
+
+def _device_outputs(dp):
+    """The step's outputs on the host, flat (plan layout) + [T] scalars."""
+    st = dp.state
+    d = dict(g8=dp.g8.cpu().numpy(), s_g=dp.s_g.cpu().numpy(), scale=dp.g_scale.cpu().numpy(),
+             mu=dp.mu.cpu().numpy(), sat=dp.sat.cpu().numpy())
+    for k in ("m1", "v", "master", "w8"):
+        s_ = getattr(st, k)
+        data = s_.data.cpu()
+        d[k] = data.view(torch.int16).numpy().view(np.uint16) if data.dtype == torch.float16 else data.numpy()
+        d[k + "_scale"] = s_.scale.cpu().numpy()
+        d[k + "_scale_inv"] = s_.scale_inv.cpu().numpy()
+        d[k + "_amax"] = s_.amax.cpu().numpy()
+    return d
+
+
+def test_c2_full_set_every_tensor(B):
+    """Config C2 (GPT-125M, 147 tensors, 123.7M params) in the bench's launch
+    configuration, EVERY tensor of every step checked against the oracle (which runs on
+    all host cores, whole tensors per worker: tests/_oracle_pool.py): 3 steps, the
+    38.6M embedding included."""
+    import synth
+    from tests._oracle_pool import OraclePool
+    specs = synth.gpt_gradient_set("gpt-125m")
+    numels = [s.numel for s in specs]
+    lr = 6e-4
+    plan = B.Plan(numels, mode=B.MODE_LOCAL, nranks=1)
+    w0 = plan.flat(torch.float32)
+    for t, v in enumerate(plan.views(w0)):
+        synth.fill_weights(v, t)
+    dp = B.FP8DataParallel(plan, w0, lr=lr)
+    pool = OraclePool(plan, w0.cpu().numpy(), lr)
+    try:
+        for step in range(1, 4):
+            g = R.make_grads(plan, 1, step, DEV)[0]
+            dp.step(g, lr=lr)
+            torch.cuda.synchronize()
+            bad = pool.check(step, g.cpu().numpy(), _device_outputs(dp))
+            assert not bad, "\n".join(bad[:10])
+    finally:
+        pool.close()
+
+
+def test_mu_reaches_cap_on_device(B):
+    """mu's growth rule (R2/R6) up to the cap on the device: tensor 1 has an all-zero
+    gradient (s_g falls back to 1, nothing saturates), so from mu = 1.996 three clean steps
+    take it to exactly 2.0 (min(2, fl(mu * fl(2^(1/1000))))) and it stays there; one huge
+    element at step 7 saturates its sum and halves it to 1.0.  Tensor 0 (synthetic data)
+    follows the oracle's mu_update on the device's saturation counts."""
+    from oracle import pipeline as OP
+    import synth
+    numels = [1000, 4096]
+    plan = B.Plan(numels, mode=B.MODE_LOCAL)
+    w0 = plan.flat(torch.float32)
+    for t, v in enumerate(plan.views(w0)):
+        synth.fill_weights(v, t)
+    dp = B.FP8DataParallel(plan, w0)
+    mu0 = F32(1.996)
+    dp.mu.fill_(float(mu0))
+    mus = [mu0, mu0]
+    for step in range(1, 9):
+        g = R.make_grads(plan, 1, step, DEV)[0]
+        g[plan.offsets[1]: plan.offsets[1] + numels[1]] = 0.0
+        if step == 7:
+            g[plan.offsets[1] + 5] = 1e30
+        dp.step(g)
+        torch.cuda.synchronize()
+        sat = dp.sat.cpu().numpy()
+        assert step == 7 or int(sat[1]) == 0
+        mus = [OP.mu_update(mus[t], int(sat[t]), numels[t], False) for t in range(2)]
+        got = [F32(x) for x in dp.mu.cpu().numpy()]
+        assert got == mus, (step, got, mus)
+        if step in (3, 4, 5, 6):
+            assert got[1] == F32(2.0), (step, got)
+        if step == 7:
+            assert got[1] == F32(1.0), got
