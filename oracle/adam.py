@@ -169,9 +169,10 @@ def bytes_per_param(master: int = 2, grad: int = 1, m1: int = 1, m2: int = 2) ->
 # observed in a certain number of preceding iterations ... necessitates the storage of a
 # history of maximum values".  Reading R25-R27: the new state scales are
 # fixed BEFORE the update, so AdamW becomes ONE pass (12 B/param instead of 18):
-#   m1 (E4M3): s_m = 448 / B_m, B_m an a-priori bound on |m'| from the current scales
-#              (|m| <= 448 m_sinv, |g| <= 448 g_sinv): never saturates (R25);
-#   v  (FP16): s_v = 65504 / B_v, B_v = beta2 65504 v_sinv + (1-beta2) (448 g_sinv)^2 (R25);
+#   m1 (E4M3): s_m = 448 / B_m, B_m = beta1 M + (1-beta1) G, M the largest dequantized m
+#              the previous step's recorded amax can give, G = 448 g_sinv the reduced
+#              gradient's ceiling: an a-priori bound on |m'|, never saturates (R25);
+#   v  (FP16): s_v = 65504 / B_v, B_v = beta2 V + (1-beta2) G^2 likewise (R25);
 #   master (FP16): s_w = 65504 / (16 H_w), w8 (E4M3): s_8 = 448 / H_w, where H_w is the
 #              maximum of the last HIST exact amax(w') values (R26; 16x headroom costs the
 #              FP16 master no precision, the w8 copy saturates like any delayed scaling).
@@ -181,16 +182,41 @@ W_HEADROOM = F32(16.0)
 BOUND_SLACK = F32(1.0 + 2.0 ** -20)    # covers the binary32 roundings of the bound itself
 
 
-def delayed_scales(st: OptState, g_scale_inv: np.float32, hp: AdamHP, w_hist) -> tuple:
-    """(s_m, s_v, s_w, s_8), each a binary32 op sequence (the kernel's, R25-R26)."""
+def delayed_moment_bounds(st: OptState, g_scale_inv: np.float32, hp: AdamHP, bound: str = "recorded"):
+    """(B_m, B_v): a-priori bounds on max|m'| and max v' before the update (R25).
+
+    bound = "recorded" (R25, the method): from the previous step's exact recorded amax
+    (R27), through the largest stored code it can produce,
+    M = fl(dec(E4M3(fl(A_m s_m))) m_sinv), V = fl(dec(F16(fl(A_v s_v))) v_sinv) (RN is
+    monotone, so every dequantized m, v is at most M, V).  Both use G = fl(448 g_sinv),
+    the saturation ceiling of the reduced gradient, and the R16 update's own op sequence,
+    so |m'| <= B_m and v' <= B_v by monotonicity; x (1 + 2^-20) as in R25.
+    bound = "prior" (round 1's reading, kept for tests/f1_headroom.py only): the format
+    ceilings |m| <= 448 m_sinv, v <= 65504 v_sinv — the previous BOUNDS, which compound
+    and start from the zero state's scale 1: 6 binades of m headroom and 30 of v on
+    average over 200 steps (profiles/r2/f1_headroom.json)."""
     gsi = F32(g_scale_inv)
-    b_m = F32(F32(F32(hp.beta1 * E4M3_MAX) * F32(st.m1.scale_inv)) +
-              F32(F32(hp.one_minus_beta1 * E4M3_MAX) * gsi))
-    b_m = F32(b_m * BOUND_SLACK)
     G = F32(E4M3_MAX * gsi)
-    b_v = F32(F32(F32(hp.beta2 * FP16_MAX) * F32(st.v.scale_inv)) +
-              F32(F32(hp.one_minus_beta2 * G) * G))
-    b_v = F32(b_v * BOUND_SLACK)
+    if bound == "prior":
+        M = F32(E4M3_MAX * F32(st.m1.scale_inv))
+        V = F32(FP16_MAX * F32(st.v.scale_inv))
+        b_m = F32(F32(F32(hp.beta1 * E4M3_MAX) * F32(st.m1.scale_inv)) +
+                  F32(F32(hp.one_minus_beta1 * E4M3_MAX) * gsi))
+        b_v = F32(F32(F32(hp.beta2 * FP16_MAX) * F32(st.v.scale_inv)) +
+                  F32(F32(hp.one_minus_beta2 * G) * G))
+    else:
+        cm = encode(np.array([F32(st.m1.amax) * F32(st.m1.scale)], np.float32), E4M3)
+        M = F32(decode_f32(cm, E4M3)[0] * F32(st.m1.scale_inv))
+        cv = encode(np.array([F32(st.v.amax) * F32(st.v.scale)], np.float32), FP16)
+        V = F32(decode_f32(cv, FP16)[0] * F32(st.v.scale_inv))
+        b_m = F32(F32(hp.beta1 * M) + F32(hp.one_minus_beta1 * G))
+        b_v = F32(F32(hp.beta2 * V) + F32(F32(hp.one_minus_beta2 * G) * G))
+    return F32(b_m * BOUND_SLACK), F32(b_v * BOUND_SLACK)
+
+
+def delayed_scales(st: OptState, g_scale_inv: np.float32, hp: AdamHP, w_hist, bound: str = "recorded") -> tuple:
+    """(s_m, s_v, s_w, s_8), each a binary32 op sequence (the kernel's, R25-R26)."""
+    b_m, b_v = delayed_moment_bounds(st, g_scale_inv, hp, bound)
     h_w = F32(np.max(np.asarray(w_hist, dtype=np.float32)))
     return (jit_scale(b_m, E4M3_MAX), jit_scale(b_v, FP16_MAX),
             jit_scale(F32(h_w * W_HEADROOM), FP16_MAX), jit_scale(h_w, E4M3_MAX))
@@ -209,13 +235,13 @@ def init_history(st: OptState) -> np.ndarray:
 
 
 def adam_step_delayed(g_hat: np.ndarray, st: OptState, hp: AdamHP, g_scale_inv: np.float32,
-                      w_hist: np.ndarray, step: int, skip: bool = False) -> Dict:
+                      w_hist: np.ndarray, step: int, skip: bool = False, bound: str = "recorded") -> Dict:
     """One FP8 AdamW step with delayed state scaling (one pass).  ``step`` >= 1 selects the
     history slot (step - 1) % HIST that receives this step's exact amax(w').
     Returns dict(state, hist, m, v, w, scales)."""
     if skip:
         return dict(state=st.copy(), hist=np.array(w_hist, np.float32), m=None, v=None, w=None)
-    s_m, s_v, s_w, s_8 = delayed_scales(st, g_scale_inv, hp, w_hist)
+    s_m, s_v, s_w, s_8 = delayed_scales(st, g_scale_inv, hp, w_hist, bound)
     g = np.asarray(g_hat, dtype=np.float32)
     m_new, v_new, w_new = adam_math(g, st.m1.value(), st.v.value(), st.master.value(), hp)
     am = F32(np.abs(m_new).max()) if m_new.size else F32(0.0)

@@ -179,3 +179,40 @@ def test_delayed_update_arithmetic_is_the_jit_one():
     b = OA.adam_step_delayed(g, st, OA.hyper_params(1e-3, 4), np.float32(1e-6), hist, 4)
     for k in ("m", "v", "w"):
         assert np.array_equal(a[k], b[k])
+
+
+def test_delayed_recorded_bound_attained_never_exceeded_and_tight():
+    """R25 (recorded-amax bound): B_m = fl(fl(b1 M) + fl((1-b1) G)) (1 + 2^-20), M the largest
+    dequantized m the recorded exact amax can give, G = fl(448 g_sinv).  Over 60 delayed
+    steps from the initial state: no m1 / v code ever saturates; in the aligned case
+    (the largest m and a code-448 gradient of the same sign at the same element) |m'| is
+    the bound's own sum, encoding at the format max and not beyond; and the headroom
+    log2(B_m / max|m'|) stays below 2 binades after the first 10 steps (the round-1
+    format-ceiling bound kept 6 on average and up to 15: profiles/r2/f1_headroom.json)."""
+    rng = np.random.default_rng(41)
+    n = 4096
+    st = OA.init_state((rng.standard_normal(n) * 0.02).astype(np.float32))
+    hist = OA.init_history(st)
+    heads = []
+    for step in range(1, 61):
+        gsi = np.float32(10.0 ** rng.uniform(-7, -6))
+        codes = rng.integers(-300, 301, size=n).astype(np.float32)
+        aligned = step > 1 and step % 5 == 0
+        if aligned:
+            i = int(np.argmax(np.abs(st.m1.value())))
+            codes[i] = 448.0 if st.m1.value()[i] >= 0 else -448.0
+        g = (decode(OA.encode(codes, E4M3), E4M3).astype(np.float32) * gsi).astype(np.float32)
+        hp = OA.hyper_params(1e-3, step)
+        b_m, b_v = OA.delayed_moment_bounds(st, gsi, hp)
+        res = OA.adam_step_delayed(g, st, hp, gsi, hist, step)
+        s_m, s_v, _, _ = res["scales"]
+        m, v = res["m"].astype(np.float64), res["v"].astype(np.float64)
+        assert np.all(np.abs(m) * s_m <= 448.0 * (1 + 2 ** -22)) and np.all(v * s_v <= 65504.0 * (1 + 2 ** -22))
+        assert np.all(np.abs(decode(res["state"].m1.codes, E4M3)) <= 448.0)
+        if aligned:      # the bound is attained (up to its slack) at the aligned element
+            assert np.abs(m).max() == np.float64(np.float32(b_m / OA.BOUND_SLACK)) or \
+                np.abs(m).max() >= float(b_m) * (1 - 2 ** -20)
+        if step > 10:
+            heads.append(math.log2(float(b_m) / np.abs(m).max()))
+        st, hist = res["state"], res["hist"]
+    assert max(heads) < 2.0, max(heads)
