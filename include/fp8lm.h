@@ -126,6 +126,13 @@ int fp8lm_zero_plan(int32_t T, const int64_t* numels, int32_t nranks,
 int fp8lm_comm_unique_id(uint8_t* id_out);
 /* Host: ncclCommInitRank on the CURRENT CUDA device.  *out receives the handle. */
 int fp8lm_comm_init(int32_t nranks, int32_t rank, const uint8_t* id, fp8lm_comm** out);
+/* Host: wrap an EXISTING NCCL communicator — e.g. torch.distributed's own, from
+ * ProcessGroupNCCL._comm_ptr() (one communicator per process, shared with
+ * the framework) — without taking ownership: fp8lm_comm_destroy then only frees the
+ * wrapper.  nccl_comm is an ncclComm_t of the NCCL library this one links (the torch-
+ * bundled libnccl.so.2, the same one torch loads); nranks / rank must match its count
+ * and rank (checked with ncclCommCount / ncclCommUserRank: EINVAL otherwise). */
+int fp8lm_comm_attach(void* nccl_comm, int32_t nranks, int32_t rank, fp8lm_comm** out);
 int fp8lm_comm_destroy(fp8lm_comm* comm);
 
 /* --------------------------------------------------------------------- the plan */
@@ -394,6 +401,11 @@ typedef struct {
 } fp8lm_commstats;
 int fp8lm_allreduce_strategy(int32_t strategy, const float* grads, int32_t nranks, int64_t n,
                              float* mu, uint8_t* codes, fp8lm_commstats* stats, void* stream);
+/* Host: the Fig. 6 metrics of one fp8lm_commstats already copied to the host (R29-R30):
+ * out3[0] = SNR in dB = 10 log10(sig2 / err2) (+inf if err2 = 0 < sig2, NaN if both are
+ * 0, -inf if sig2 = 0 < err2); out3[1] = underflow rate = underflow / events; out3[2] =
+ * overflow rate = overflow / events (0 when events = 0).  EINVAL on NULL pointers. */
+int fp8lm_commstats_metrics(const fp8lm_commstats* host_stats, double* out3);
 
 /* ------------------ (8) FP8 sequence/tensor-parallel activation converter g (f4) */
 /* PAPER.md §2.3, Fig. 5: "We add an FP8 datatype conversion prior to g, such

@@ -61,6 +61,8 @@ _sig("fp8lm_zero_plan", C.c_int, _i32, C.POINTER(_i64), _i32, C.POINTER(_i32), C
 _sig("fp8lm_comm_unique_id", C.c_int, C.POINTER(C.c_uint8))
 _sig("fp8lm_comm_init", C.c_int, _i32, _i32, C.POINTER(C.c_uint8), C.POINTER(_p))
 _sig("fp8lm_comm_destroy", C.c_int, _p)
+_sig("fp8lm_comm_attach", C.c_int, _p, _i32, _i32, C.POINTER(_p))
+_sig("fp8lm_commstats_metrics", C.c_int, _p, C.POINTER(C.c_double))
 _sig("fp8lm_plan_create", C.c_int, _i32, C.POINTER(_i64), _i32, _i32, _i32, C.POINTER(_p))
 _sig("fp8lm_plan_destroy", C.c_int, _p)
 _sig("fp8lm_plan_offset", _i64, _p, _i32)
@@ -207,9 +209,26 @@ class Comm:
         return bytes(buf)
 
     @classmethod
-    def from_torch_distributed(cls, group=None) -> "Comm":
+    def from_torch_distributed(cls, group=None, attach: bool = True) -> "Comm":
+        """attach=True: wrap torch.distributed's own NCCL communicator of `group`
+        (ProcessGroupNCCL._comm_ptr(), fp8lm_comm_attach: one communicator per process);
+        False, or when torch's communicator is not available: a new one of the library's
+        own, bootstrapped over torch.distributed."""
         import torch.distributed as dist
         rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if attach:
+            try:
+                pg = group if group is not None else dist.distributed_c10d._get_default_group()
+                backend = pg._get_backend(torch.device("cuda", torch.cuda.current_device()))
+                ptr = backend._comm_ptr()
+            except Exception:
+                ptr = 0
+            if ptr:
+                obj = cls.__new__(cls)
+                h = _p()
+                _check(lib.fp8lm_comm_attach(C.c_void_p(ptr), world, rank, C.byref(h)), "fp8lm_comm_attach")
+                obj.handle, obj.nranks, obj.rank, obj.attached = h, world, rank, True
+                return obj
         obj: List[Optional[bytes]] = [cls.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0, group=group)
         return cls(world, rank, obj[0])
@@ -488,11 +507,10 @@ def commstats_read(buf: torch.Tensor) -> dict:
     keys = ("sig2", "err2", "underflow", "overflow", "events", "sat", "nonfinite", "amax", "s",
             "scale", "scale_inv", "mu_used", "mu_next")
     d = dict(zip(keys, v[:13]))
-    d["underflow_rate"] = d["underflow"] / d["events"] if d["events"] else 0.0
-    d["overflow_rate"] = d["overflow"] / d["events"] if d["events"] else 0.0
-    e, g = d["err2"], d["sig2"]
-    d["snr_db"] = (float("inf") if g > 0 else float("nan")) if e == 0 else (
-        10.0 * math.log10(g / e) if g > 0 else float("-inf"))
+    raw = (C.c_uint8 * COMMSTATS_BYTES).from_buffer_copy(buf.detach().cpu().numpy().tobytes())
+    out = (C.c_double * 3)()
+    _check(lib.fp8lm_commstats_metrics(C.cast(raw, _p), out), "fp8lm_commstats_metrics")
+    d["snr_db"], d["underflow_rate"], d["overflow_rate"] = out[0], out[1], out[2]
     return d
 
 

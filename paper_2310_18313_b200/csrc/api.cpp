@@ -59,6 +59,7 @@ struct fp8lm_comm {
 #endif
   int32_t nranks = 0;
   int32_t rank = 0;
+  bool owned = true;         // false: attached (fp8lm_comm_attach), not destroyed here
 };
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -158,10 +159,44 @@ int fp8lm_comm_init(int32_t nranks, int32_t rank, const uint8_t* id, fp8lm_comm*
 #endif
 }
 
+int fp8lm_comm_attach(void* nccl_comm, int32_t nranks, int32_t rank, fp8lm_comm** out) {
+#ifdef FP8LM_WITH_NCCL
+  if (!nccl_comm || !out || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(FP8LM_EINVAL, "comm_attach: bad arguments (nranks=%d rank=%d)", nranks, rank);
+  ncclComm_t c = static_cast<ncclComm_t>(nccl_comm);
+  int cnt = -1, rk = -1;
+  NCCL_TRY(ncclCommCount(c, &cnt));
+  NCCL_TRY(ncclCommUserRank(c, &rk));
+  if (cnt != nranks || rk != rank)
+    return fail(FP8LM_EINVAL, "comm_attach: communicator is rank %d of %d, expected %d of %d", rk, cnt,
+                rank, nranks);
+  auto* w = new fp8lm_comm();
+  w->comm = c;
+  w->nranks = nranks;
+  w->rank = rank;
+  w->owned = false;
+  *out = w;
+  return FP8LM_OK;
+#else
+  (void)nccl_comm; (void)nranks; (void)rank; (void)out;
+  return fail(FP8LM_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+int fp8lm_commstats_metrics(const fp8lm_commstats* st, double* out3) {
+  if (!st || !out3) return fail(FP8LM_EINVAL, "commstats_metrics: NULL");
+  const double g = st->sig2, e = st->err2;
+  if (e == 0.0) out3[0] = g > 0.0 ? HUGE_VAL : NAN;
+  else out3[0] = g > 0.0 ? 10.0 * std::log10(g / e) : -HUGE_VAL;
+  out3[1] = st->events ? (double)st->underflow / (double)st->events : 0.0;
+  out3[2] = st->events ? (double)st->overflow / (double)st->events : 0.0;
+  return FP8LM_OK;
+}
+
 int fp8lm_comm_destroy(fp8lm_comm* comm) {
   if (!comm) return FP8LM_OK;
 #ifdef FP8LM_WITH_NCCL
-  if (comm->comm) {
+  if (comm->comm && comm->owned) {
     ncclCommFinalize(comm->comm);
     ncclCommDestroy(comm->comm);
   }

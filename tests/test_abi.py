@@ -171,3 +171,21 @@ def test_sass_paired_fp32_has_no_contracted_products(B):
     for fn, c in counts.items():
         assert fn.startswith("_ZN5fp8lm6k_adamILi2E"), (fn, c)
         assert c == 48, (fn, c)
+
+
+def test_commstats_metrics_host(B):
+    """fp8lm_commstats_metrics (R29-R30): SNR = 10 log10(sig2 / err2) and the event rates."""
+    import struct
+    import ctypes as C
+    import math
+    def metrics(sig2, err2, under, over, events):
+        raw = struct.pack("<ddQQQIIffffff4I", sig2, err2, under, over, events, 0, 0, *([0.0] * 6), 0, 0, 0, 0)
+        buf = (C.c_uint8 * len(raw)).from_buffer_copy(raw)
+        out = (C.c_double * 3)()
+        assert B.lib.fp8lm_commstats_metrics(C.cast(buf, C.c_void_p), out) == 0
+        return list(out)
+    snr, u, o = metrics(100.0, 1.0, 3, 1, 1000)
+    assert snr == 20.0 and u == 0.003 and o == 0.001
+    assert metrics(1.0, 0.0, 0, 0, 0)[0] == math.inf and metrics(1.0, 0.0, 0, 0, 0)[1:] == [0.0, 0.0]
+    assert math.isnan(metrics(0.0, 0.0, 0, 0, 10)[0])
+    assert metrics(0.0, 2.0, 0, 0, 10)[0] == -math.inf
