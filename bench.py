@@ -55,10 +55,11 @@ def parse():
                     help="N > 1: fused peer-memory reduce-scatter/all-gather kernel (p2p), "
                          "NCCL all-to-all + all-gather around the reduce kernel (nccl), or "
                          "FP8 ZeRO whole-tensor owners over peer memory (zero, config C4)")
-    ap.add_argument("--buckets", type=int, default=1,
+    ap.add_argument("--buckets", type=int, default=0,
                     help="N > 1, modes p2p / zero: split the tensors into this many buckets (one plan "
                          "each) and run the step in two phases per bucket (fp8lm_dp_step_split), so "
-                         "the exchange of one bucket overlaps the HBM passes of the others")
+                         "the exchange of one bucket overlaps the HBM passes of the others.  0 = auto: "
+                         "6 for sets above 1G params, else 1 (small sets are launch-bound)")
     ap.add_argument("--lr", type=float, default=0.0,
                     help="0: the paper's max LR of the config (Table 1, P:279-282: 6e-4 for "
                          "GPT-125M, 3e-4 for 7B, 13B and C1, 6e-5 for 175B)")
@@ -414,7 +415,9 @@ def main():
     mode = ({"p2p": B.MODE_P2P, "nccl": B.MODE_NCCL, "zero": B.MODE_ZERO}[args.exchange]
             if N > 1 else (B.MODE_SIMULATED if sim else B.MODE_LOCAL))
     zero = mode == B.MODE_ZERO
-    nb = args.buckets if (N > 1 and args.exchange in ("p2p", "zero")) else 1
+    nb = args.buckets if args.buckets > 0 else (6 if params > 1e9 else 1)
+    if not (N > 1 and args.exchange in ("p2p", "zero")):
+        nb = 1
     groups = B.bucket_split(numels, nb) if nb > 1 else [list(range(len(numels)))]
     plans = [B.Plan([numels[t] for t in grp], mode=mode, nranks=sim or N, rank=rank) for grp in groups]
     plan = plans[0] if nb == 1 else None

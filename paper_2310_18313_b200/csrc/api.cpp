@@ -982,6 +982,30 @@ static int split_resources(fp8lm_plan* p) {
   return FP8LM_OK;
 }
 
+// Split-step grid caps: the exchange kernel of phase 1 runs at 1.5 CTAs per SM (its
+// launch bounds keep it <= 85 registers, 3 CTAs/SM possible), so that it is resident
+// beside the HBM passes of the other buckets instead of taking every slot (highest
+// stream priority) and serialising them; FP8LM_SPLIT_HCAP (CTAs per SM, 0 = off) caps the
+// HBM passes as well.  Measured at GPT-7B N = 4 with 4 buckets (profiles/r2/split):
+// 1 CTA/SM 29.5 ms, 1.25 30.0, 1.5 28.8, 2 28.5-30.0, uncapped 33.8, unsplit 31.5.
+#ifndef FP8LM_SPLIT_XCAP
+#define FP8LM_SPLIT_XCAP 0           /* 0: 3 * #SMs / 2 */
+#endif
+#ifndef FP8LM_SPLIT_HCAP
+#define FP8LM_SPLIT_HCAP 0
+#endif
+static int split_xcap(const fp8lm_plan* p) {
+  if (p->loopback_ctas) return p->loopback_ctas;
+  return FP8LM_SPLIT_XCAP ? FP8LM_SPLIT_XCAP : 3 * num_sms() / 2;
+}
+struct CapScope {
+  LaunchPolicy saved;
+  explicit CapScope(int ctas) : saved(launch_policy()) {
+    if (ctas > 0 && (saved.max_ctas == 0 || ctas < saved.max_ctas)) launch_policy().max_ctas = ctas;
+  }
+  ~CapScope() { launch_policy() = saved; }
+};
+
 // phase 0: the whole step on `stream`; 1: amax + quantize on `stream`, the exchange kernel
 // on the plan's exchange stream; 2: `stream` waits for that exchange, then the AdamW pass
 static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
@@ -991,6 +1015,7 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
                         const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
                         int32_t hist_slot, void* stream, int phase) {
   const LaunchScope ls_(p);   // loopback plans: capped grids
+  const CapScope hcap_(phase ? FP8LM_SPLIT_HCAP * num_sms() : 0);
   int rc;
   if (phase != 2 && (rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream)))
     return rc;
@@ -1029,8 +1054,14 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
         CUDA_TRY(cudaStreamWaitEvent(p->xs, p->ev_q, 0));
         xs = p->xs;
       }
-      CUDA_TRY(launch_reduce_owner_a1(p->dev, p->own->dev, p2p_args(p, p->epoch), s_g, tail, g8, *m1, *v,
-                                      *master, *w8, *hp, skip, xs));
+      {
+        LaunchPolicy keep = launch_policy();
+        if (phase == 1) launch_policy().max_ctas = split_xcap(p);
+        rc = launch_reduce_owner_a1(p->dev, p->own->dev, p2p_args(p, p->epoch), s_g, tail, g8, *m1, *v,
+                                    *master, *w8, *hp, skip, xs);
+        launch_policy() = keep;
+        CUDA_TRY((cudaError_t)rc);
+      }
       if (phase == 1) {
         CUDA_TRY(cudaEventRecord(p->ev_x, p->xs));
         return FP8LM_OK;
@@ -1076,10 +1107,16 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
         CUDA_TRY(cudaStreamWaitEvent(p->xs, p->ev_q, 0));
         xs = p->xs;
       }
-      if (delayed)            // reduce-scatter only (the single delayed pass pulls the rest)
-        CUDA_TRY(launch_reduce_p2p(p->dev, x, g8, s_g, tail, xs, /*ag=*/false));
-      else
-        CUDA_TRY(launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip, xs));
+      {
+        LaunchPolicy keep = launch_policy();
+        if (phase == 1) launch_policy().max_ctas = split_xcap(p);
+        if (delayed)            // reduce-scatter only (the single delayed pass pulls the rest)
+          rc = launch_reduce_p2p(p->dev, x, g8, s_g, tail, xs, /*ag=*/false);
+        else
+          rc = launch_reduce_p2p_a1(p->dev, x, s_g, tail, g8, *m1, *v, *master, *w8, *hp, skip, xs);
+        launch_policy() = keep;
+        CUDA_TRY((cudaError_t)rc);
+      }
       if (phase == 1) {
         CUDA_TRY(cudaEventRecord(p->ev_x, p->xs));
         return FP8LM_OK;
