@@ -4,8 +4,10 @@ NCCL bf16, under torchrun on N GPUs of one box.
 
 For every FP8 payload size n (bytes = elements) it times, max over ranks, CUDA events:
   p2p_full  — amax_scale_sync + fp8_grad_allreduce in mode P2P from an fp32 gradient
-              (amax, MIN of scales through peer pads, quantize, fused peer-memory
-              reduce-scatter + rank-order reduce + all-gather)
+              (amax, MIN of scales through peer pads, then up to 1 MiB the one-shot
+              exchange kernel, above it quantize + the fused peer-memory reduce-scatter +
+              rank-order reduce + all-gather)
+  p2p_rsag_full — up to 1 MiB: the same with the one-shot path off (quantize + RS + AG)
   p2p_xchg  — the fused exchange kernel alone (k_reduce_p2p, library launch tracing)
   nccl_full — the same arithmetic with NCCL transport (mode NCCL)
   nccl_bf16 — torch.distributed.all_reduce of n bf16 elements (NCCL, default algorithm)
@@ -67,9 +69,13 @@ def main():
         g = torch.empty(n, dtype=torch.float32, device="cuda")
         synth.fill_gradient(g, 1, 0, rank, amp=1e-3)
         res = {}
-        for mode_name, mode in (("p2p", B.MODE_P2P), ("nccl", B.MODE_NCCL)):
+        for mode_name, mode, oneshot in (("p2p", B.MODE_P2P, True), ("p2p_rsag", B.MODE_P2P, False),
+                                         ("nccl", B.MODE_NCCL, False)):
+            if mode_name == "p2p_rsag" and n > (1 << 20):
+                continue                       # above 1 MiB both p2p rows are the RS+AG path
             plan = B.Plan([n], mode=mode, nranks=N, rank=rank)
             if mode == B.MODE_P2P:
+                plan.set_oneshot((1 << 20) if oneshot else 0)
                 plan.peer_setup(comm)
                 g8 = plan.peer_g8()
                 c = None
@@ -88,11 +94,12 @@ def main():
                 B.amax_scale_sync(plan, g, mu, amax, s_g, skip, comm=c)
                 B.fp8_grad_allreduce(plan, g, s_g, skip, g8, gs, gsi, sat, mu, comm=c)
 
-            B.prof_enable(True)
             res[f"{mode_name}_full"] = timed(full, iters)
+            B.prof_enable(True)                  # a second, instrumented pass for the kernel
+            timed(full, iters)
             B.prof_enable(False)
             prof = B.prof_read()
-            if mode == B.MODE_P2P and "reduce_p2p" in prof:
+            if mode_name == "p2p" and "reduce_p2p" in prof:
                 t = torch.tensor([prof["reduce_p2p"]["ms"] / prof["reduce_p2p"]["launches"]],
                                  dtype=torch.float64, device="cuda")
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)

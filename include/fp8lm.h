@@ -198,6 +198,16 @@ int fp8lm_peer_setup_loopback(fp8lm_plan* const* plans, int32_t n, void* stream)
 int fp8lm_set_peer_timeout(double seconds);
 int fp8lm_peer_timeout_report(uint32_t* out4);
 
+/* Mode P2P, small messages: a plan whose reduced-code buffer (fp8lm_plan_g8_bytes) is at
+ * most max_bytes (default 1 MiB; 0 = never) exchanges with the ONE-SHOT kernel instead of
+ * quantize + reduce-scatter + all-gather: it quantizes into the own send window, meets the
+ * ranks at one flag, and every rank pulls and reduces the whole set from every rank
+ * (rank order, R12) — the same results with one kernel and one cross-rank handshake,
+ * (N-1) n bytes of NVLink per rank instead of 2 (N-1)/N n (config C5's small sizes).
+ * fp8lm_grad_allreduce and fp8lm_dp_step (not the split step); every rank must set the
+ * same value.  Host call; EINVAL on a NULL plan or a negative size. */
+int fp8lm_plan_set_oneshot(fp8lm_plan* plan, int64_t max_bytes);
+
 /* Mode P2P: this rank's g8 window (device); pass it as g8 to the calls below.  NULL if
  * fp8lm_peer_setup has not run. */
 uint8_t* fp8lm_peer_g8(const fp8lm_plan* plan);

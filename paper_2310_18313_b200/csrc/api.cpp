@@ -500,6 +500,12 @@ float* fp8lm_peer_w8_scalars(const fp8lm_plan* p) {
                                   (size_t)p->nranks * p->T * 8);
 }
 
+int fp8lm_plan_set_oneshot(fp8lm_plan* p, int64_t max_bytes) {
+  if (!p || max_bytes < 0) return fail(FP8LM_EINVAL, "plan_set_oneshot: bad arguments");
+  p->oneshot_max_bytes = max_bytes;
+  return FP8LM_OK;
+}
+
 int64_t fp8lm_plan_offset(const fp8lm_plan* p, int32_t t) {
   if (!p || t < 0 || t >= p->T) return -1;
   return p->offset[t];
@@ -861,6 +867,10 @@ int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int
     CUDA_TRY(launch_reduce_owner(d, p->own->dev, p2p_args(p, p->epoch), g8, s_g, tail, s));
   } else if (p->mode == FP8LM_MODE_P2P) {
     if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "grad_allreduce: mode P2P needs g8 == fp8lm_peer_g8(plan)");
+    if (p->g8_bytes <= p->oneshot_max_bytes) {   // small message: one kernel, one handshake
+      CUDA_TRY(launch_oneshot(d, p2p_args(p, p->epoch), srcs[0], src_dtype, g8, s_g, tail, s));
+      return FP8LM_OK;
+    }
     uint8_t* dst[1] = {p->win_send};
     CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, nullptr, s));
     // A4 + A5 in one kernel over NVLink peer memory (same epoch as this step's amax)
@@ -1095,6 +1105,20 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
     if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "dp_step: mode P2P needs g8 == fp8lm_peer_g8(plan)");
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
     P2PArgs x = p2p_args(p, p->epoch);
+    if (phase == 0 && p->g8_bytes <= p->oneshot_max_bytes) {
+      // small message: the one-shot exchange leaves the whole reduced set in g8, so both
+      // AdamW passes run locally (no pull)
+      const void* srcs[1];
+      int nsrc = 0;
+      if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
+      CUDA_TRY(launch_oneshot(p->dev, x, srcs[0], src_dtype, g8, s_g, tail, S(stream)));
+      if (delayed)
+        CUDA_TRY(launch_adam_delayed(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, w_hist,
+                                     hist_slot, S(stream)));
+      else
+        CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream)));
+      return FP8LM_OK;
+    }
     if (phase != 2) {
       const void* srcs[1];
       int nsrc = 0;

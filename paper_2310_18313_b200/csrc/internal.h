@@ -46,7 +46,8 @@ struct DevPlan {
   float* gsinv_own;         // [T_own] compact copy of g_scale_inv (written by the reduce tail)
 };
 
-constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2, kCtrFix = 3, kCtrFixGen = 4, kCtrWords = 8;
+constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2, kCtrFix = 3, kCtrFixGen = 4, kCtrOneshot = 5,
+              kCtrWords = 8;
 
 // ---------------------------------------------------------------- mode P2P windows
 // Signal / exchange pad of one rank (bytes): three flag arrays (one u32 epoch slot per
@@ -158,6 +159,9 @@ struct fp8lm_plan {
   // loopback_ctas CTAs (num_sms / N, so the N ranks' kernels are all resident at once:
   // the spin-waits need that) without the cooperative / PDL attributes.  0: off.
   int loopback_ctas = 0;
+  // mode P2P: a plan whose reduced codes fit in this many bytes takes the one-shot
+  // exchange (fp8lm_plan_set_oneshot; default 1 MiB)
+  int64_t oneshot_max_bytes = 1 << 20;
   // split step (fp8lm_dp_step_split): the exchange stream and its two events
   cudaStream_t xs = nullptr;
   cudaEvent_t ev_q = nullptr, ev_x = nullptr;
@@ -196,6 +200,10 @@ cudaError_t launch_amax(const DevPlan& p, const void* const* srcs, int nsrc, int
                         bool finalize, const P2PArgs* x, cudaStream_t s);
 cudaError_t launch_reduce_p2p(const DevPlan& p, const P2PArgs& x, uint8_t* g8, const float* s_g,
                               const TailArgs& tail, cudaStream_t s, bool ag = true);
+// mode P2P, small messages: quantize into the own send window, then every rank pulls and
+// reduces the WHOLE tensor set from every rank (one kernel, one cross-rank handshake)
+cudaError_t launch_oneshot(const DevPlan& p, const P2PArgs& x, const void* src, int src_dtype,
+                           uint8_t* g8, const float* s_g, const TailArgs& tail, cudaStream_t s);
 // mode ZERO: owner reduce over the compact sub-plan `o` (items), tails on the full plan `p`
 cudaError_t launch_reduce_owner(const DevPlan& p, const DevPlan& o, const P2PArgs& x, uint8_t* g8,
                                 const float* s_g, const TailArgs& tail, cudaStream_t s);

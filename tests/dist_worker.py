@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--unfused", action="store_true",
                     help="the three ABI calls instead of fp8lm_dp_step")
     ap.add_argument("--delayed", action="store_true", help="delayed state scaling (R25-R27)")
+    ap.add_argument("--oneshot", action="store_true", help="mode P2P: the one-shot small-message exchange")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -47,6 +48,7 @@ def main():
     comm = B.Comm.from_torch_distributed()
     mode = {"p2p": B.MODE_P2P, "nccl": B.MODE_NCCL, "zero": B.MODE_ZERO}[args.mode]
     plan = B.Plan(NUMELS, mode=mode, nranks=N, rank=rank)
+    plan.set_oneshot(1 << 40 if args.oneshot else 0)
     w0 = plan.flat(torch.float32)
     for t, v in enumerate(plan.views(w0)):
         synth.fill_weights(v, t)
@@ -76,7 +78,7 @@ def main():
                             step=step)
         if args.delayed:
             hists = res["hists"]
-        for m in R.compare_rank(B, plan, dp, res, rank, args.mode, not args.unfused):
+        for m in R.compare_rank(B, plan, dp, res, rank, args.mode, not args.unfused and not args.oneshot):
             ok = False
             msgs.append(f"step {step}: {m}")
         mus = res["mu_next"]
@@ -86,7 +88,8 @@ def main():
     for m in msgs[:10]:
         print(m, flush=True)
     if rank == 0:
-        tag = args.mode.upper() + ("_UNFUSED" if args.unfused else "") + ("_DELAYED" if args.delayed else "")
+        tag = args.mode.upper() + ("_UNFUSED" if args.unfused else "") + ("_DELAYED" if args.delayed else "") + \
+            ("_ONESHOT" if args.oneshot else "")
         print(f"{tag} parity N={N}: {'OK' if flag.item() == 1 else 'MISMATCH'}", flush=True)
     comm.close()
     dist.destroy_process_group()

@@ -48,10 +48,14 @@ def B():
 
 
 def run_loopback(B, numels, mode, N, steps, fused=True, delayed=False, lr=3e-4, sub=None,
-                 specials=None):
+                 specials=None, oneshot=False):
+    """oneshot: mode P2P's small-message exchange (fp8lm_plan_set_oneshot); off by
+    default so that these small sets take the reduce-scatter / all-gather kernels."""
     import synth
     bmode = {"p2p": B.MODE_P2P, "zero": B.MODE_ZERO}[mode]
     plans = [B.Plan(numels, mode=bmode, nranks=N, rank=r) for r in range(N)]
+    for p_ in plans:
+        p_.set_oneshot(1 << 40 if oneshot else 0)
     B.peer_setup_loopback(plans)
     streams = [torch.cuda.Stream() for _ in range(N)]
     w0 = plans[0].flat(torch.float32)
@@ -86,7 +90,8 @@ def run_loopback(B, numels, mode, N, steps, fused=True, delayed=False, lr=3e-4, 
                     for g in grads]
         res = OS.train_step(per_rank, mus, ref_states, OA.hyper_params(lr, step), hists=hists, step=step)
         for r in range(N):
-            msgs += [f"step {step}: {m}" for m in R.compare_rank(B, plans[r], dps[r], res, r, mode, fused, sub)]
+            msgs += [f"step {step}: {m}" for m in
+                     R.compare_rank(B, plans[r], dps[r], res, r, mode, fused and not oneshot, sub)]
         assert not msgs, "\n".join(msgs[:10])
         mus = res["mu_next"]
         ref_states = res["states"]
@@ -109,6 +114,16 @@ def test_loopback_bit_exact(B, N, variant):
     mode = variant.split("_")[0]
     run_loopback(B, RAGGED, mode, N, steps=3, fused="unfused" not in variant,
                  delayed="delayed" in variant, specials=_huge)
+
+
+@pytest.mark.parametrize("N", [2, 3, 4])
+@pytest.mark.parametrize("variant", ["fused", "unfused", "delayed"])
+def test_loopback_oneshot(B, N, variant):
+    """Mode P2P's one-shot small-message exchange (k_oneshot: quantize, one handshake,
+    every rank pulls and reduces the whole set): bit-exact through fp8lm_dp_step (then
+    both AdamW passes locally), the three calls and delayed scaling."""
+    run_loopback(B, RAGGED, "p2p", N, steps=3, fused=variant != "unfused", delayed=variant == "delayed",
+                 specials=_huge, oneshot=True)
 
 
 @pytest.mark.parametrize("mode", ["p2p", "zero"])
