@@ -60,6 +60,9 @@ def parse():
                          "each) and run the step in two phases per bucket (fp8lm_dp_step_split), so "
                          "the exchange of one bucket overlaps the HBM passes of the others.  0 = auto: "
                          "6 for sets above 1G params, else 1 (small sets are launch-bound)")
+    ap.add_argument("--bucket-lag", type=int, default=0,
+                    help="split step issue order: 0 = phase 1 of every bucket then phase 2 of every "
+                         "bucket; k = phase 2 of bucket b after phase 1 of bucket b + k")
     ap.add_argument("--lr", type=float, default=0.0,
                     help="0: the paper's max LR of the config (Table 1, P:279-282: 6e-4 for "
                          "GPT-125M, 3e-4 for 7B, 13B and C1, 6e-5 for 175B)")
@@ -450,7 +453,8 @@ def main():
     grads = gsets[0]
     delayed = args.state_scaling == "delayed"
     if nb > 1:
-        dp = B.BucketedDP(plans, w0s, comm=comm, lr=args.lr, state_scaling=args.state_scaling)
+        dp = B.BucketedDP(plans, w0s, comm=comm, lr=args.lr, state_scaling=args.state_scaling,
+                          lag=args.bucket_lag)
     else:
         dp = B.FP8DataParallel(plans[0], w0s[0], comm=comm, lr=args.lr, state_scaling=args.state_scaling)
     dps = dp.dps if nb > 1 else [dp]
@@ -653,7 +657,7 @@ def main():
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": WORKLOAD[args.config] + (", ZeRO owner mode (Alg. 1)" if zero else ""),
                        "tensors": len(numels), "params": params, "grad_dtype": args.dtype,
-                       "buckets": nb, "lr": args.lr,
+                       "buckets": nb, "bucket_lag": args.bucket_lag, "lr": args.lr,
                        "case": "worst (amax(w') screen fallback)" if args.worst_case else "typical",
                        "alg_bytes_per_param_per_rank": bytes_rank / params,
                        "parallelism": f"dp{N}" if N > 1 else (f"{sim} simulated ranks" if sim else "single"), "state_scaling": args.state_scaling,

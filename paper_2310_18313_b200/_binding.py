@@ -715,12 +715,22 @@ class BucketedDP:
     so the exchange of bucket b runs on its exchange stream beside the amax / quantize of
     bucket b+1 and the AdamW pass of bucket b-1 on the caller's stream."""
 
-    def __init__(self, plans: Sequence[Plan], w0s: Sequence[torch.Tensor], comm: Comm = None, **kw):
+    def __init__(self, plans: Sequence[Plan], w0s: Sequence[torch.Tensor], comm: Comm = None,
+                 lag: int = 0, **kw):
+        """lag: 0 = phase 1 of every bucket, then phase 2 of every bucket; k > 0 = phase 2 of
+        bucket b is issued after phase 1 of bucket b + k (a software pipeline of depth k)."""
         self.plans = list(plans)
+        self.lag = lag
         self.dps = [FP8DataParallel(p, w, comm=comm, **kw) for p, w in zip(self.plans, w0s)]
 
     def step(self, grads: Sequence[torch.Tensor], lr: float = None, stream=None):
-        for dp, g in zip(self.dps, grads):
+        B = len(self.dps)
+        lag = self.lag if self.lag > 0 else B
+        done = 0
+        for b, (dp, g) in enumerate(zip(self.dps, grads)):
             dp.step_begin(g, lr, stream)
-        for dp in self.dps:
+            if b - done >= lag:
+                self.dps[done].step_end(stream)
+                done += 1
+        for dp in self.dps[done:]:
             dp.step_end(stream)

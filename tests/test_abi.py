@@ -152,9 +152,11 @@ def test_sass_paired_fp32_has_no_contracted_products(B):
     FP32 bodies (device.cuh P2: FMUL2 / FFMA2) keep additions scalar because ptxas
     contracts a mul.rn.f32x2 feeding an add.rn.f32x2 into an FFMA2 even under
     --fmad=false; the only FFMA2 allowed are the 6 per lane pair inside the paired
-    sqrt / division cores (2 + 4), i.e. 48 per 16-element group body, and only in the
-    kernels that contain that body (k_adam<2, .>).  A contracted product would show up
-    as extra FFMA2 here (and as a parity failure on the GPU)."""
+    sqrt / division cores (2 + 4), i.e. 48 per 16-element group body: pass 2's body
+    (k_adam<2, .>) and pass 1's certified exact screen (screen_exact_p2, in every kernel
+    that runs pass 1: k_adam<1>, k_adam<3, ., ., NS>, the exchange kernels), one body per
+    kernel.  A contracted product would show up as extra FFMA2 here (and as a parity
+    failure on the GPU)."""
     import shutil
     import subprocess
     tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
@@ -168,9 +170,12 @@ def test_sass_paired_fp32_has_no_contracted_products(B):
         elif "FFMA2" in line and fn:
             counts[fn] = counts.get(fn, 0) + 1
     assert counts, "no FFMA2 at all: the paired pass-2 body is missing"
+    allowed = ("_ZN5fp8lm6k_adamILi1E", "_ZN5fp8lm6k_adamILi2E", "_ZN5fp8lm6k_adamILi3E",
+               "_ZN5fp8lm15k_reduce_p2p_a1", "_ZN5fp8lm17k_reduce_owner_a1")
     for fn, c in counts.items():
-        assert fn.startswith("_ZN5fp8lm6k_adamILi2E"), (fn, c)
+        assert fn.startswith(allowed), (fn, c)
         assert c == 48, (fn, c)
+    assert any(fn.startswith("_ZN5fp8lm6k_adamILi2E") for fn in counts)
 
 
 def test_commstats_metrics_host(B):
