@@ -519,6 +519,16 @@ def commstats_read(buf: torch.Tensor) -> dict:
     return d
 
 
+def commstats_metrics(sig2: float, err2: float, underflow: int, overflow: int, events: int):
+    """fp8lm_commstats_metrics on aggregated sums (several calls' statistics added up):
+    -> (snr_db, underflow_rate, overflow_rate)."""
+    raw = _COMMSTATS.pack(sig2, err2, underflow, overflow, events, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0)
+    buf = (C.c_uint8 * len(raw)).from_buffer_copy(raw)
+    out = (C.c_double * 3)()
+    _check(lib.fp8lm_commstats_metrics(C.cast(buf, _p), out), "fp8lm_commstats_metrics")
+    return out[0], out[1], out[2]
+
+
 def allreduce_strategy(grads: torch.Tensor, strategy, mu: torch.Tensor = None,
                        codes: torch.Tensor = None, stats: torch.Tensor = None, stream=None):
     """fp8lm_allreduce_strategy: N ranks' gradients as rows of a [N, n] fp32 device tensor;

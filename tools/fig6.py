@@ -38,12 +38,26 @@ def student_t3(shape, gen, dev):
     return z / torch.sqrt(chi / 3.0)
 
 
-def draw(out, N, n, rho, seed):
+def draw(out, N, n, rho, seed, dist="t3", sigma=2.0):
+    """t3: a (rho c + sqrt(1-rho^2) z_r), c, z_r ~ Student-t(3).
+    lognormal: magnitudes a exp(sigma (rho c + sqrt(1-rho^2) z_r)) with signs
+    sign(rho u + sqrt(1-rho^2) v_r), c, z_r, u, v_r ~ N(0, 1): correlated log-normal
+    magnitudes and correlated signs across ranks, sigma = the spread in natural-log units."""
     gen = torch.Generator(device=out.device)
     gen.manual_seed(seed)
-    c = student_t3((n,), gen, out.device)
-    z = student_t3((N, n), gen, out.device)
-    out.copy_(z.mul_(math.sqrt(1.0 - rho * rho)).add_(c.mul_(rho)).mul_(1e-3))
+    k = math.sqrt(1.0 - rho * rho)
+    if dist == "t3":
+        c = student_t3((n,), gen, out.device)
+        z = student_t3((N, n), gen, out.device)
+        out.copy_(z.mul_(k).add_(c.mul_(rho)).mul_(1e-3))
+        return
+    c = torch.randn((n,), generator=gen, device=out.device)
+    z = torch.randn((N, n), generator=gen, device=out.device)
+    u = torch.randn((n,), generator=gen, device=out.device)
+    v = torch.randn((N, n), generator=gen, device=out.device)
+    mag = z.mul_(k).add_(c.mul_(rho)).mul_(sigma).exp_().mul_(1e-5)
+    sgn = torch.sign(v.mul_(k).add_(u.mul_(rho)))
+    out.copy_(mag.mul_(sgn))
 
 
 def main():
@@ -52,6 +66,8 @@ def main():
     ap.add_argument("--n", type=int, default=1 << 22)
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--blocks", default="0,4,8,12,16,20,24,28,31")
+    ap.add_argument("--dist", default="t3", choices=["t3", "lognormal"])
+    ap.add_argument("--sigma", type=float, default=2.0)
     args = ap.parse_args()
     import paper_2310_18313_b200 as B
     dev = torch.device("cuda")
@@ -69,7 +85,7 @@ def main():
         for ti, name in enumerate(TENSORS):
             mu = torch.ones(1, device=dev)
             for step in range(args.steps):
-                draw(g, N, n, rho, seed=(b * 16 + ti) * 1000 + step)
+                draw(g, N, n, rho, seed=(b * 16 + ti) * 1000 + step, dist=args.dist, sigma=args.sigma)
                 last = step == args.steps - 1
                 for strat in (("pre", "post", "auto") if last else ("auto",)):
                     torch.cuda.synchronize()
@@ -86,11 +102,13 @@ def main():
                         if strat == "auto":
                             mus.append(d["mu_used"])
         for strat, a in agg.items():
-            snr = 10 * math.log10(a["sig2"] / a["err2"]) if a["err2"] > 0 else float("inf")
+            # the metrics of the summed statistics, computed by the library (R29-R30)
+            snr, ur, orate = B.commstats_metrics(a["sig2"], a["err2"], int(a["underflow"]), int(a["overflow"]),
+                                                 int(a["events"]))
             row = {"fig": 6, "model": "gpt-7b", "block": b, "rho": round(rho, 4), "dp": N,
-                   "n_per_tensor": n, "tensors": list(TENSORS), "strategy": strat,
-                   "snr_db": snr, "underflow_rate": a["underflow"] / a["events"],
-                   "overflow_rate": a["overflow"] / a["events"]}
+                   "n_per_tensor": n, "tensors": list(TENSORS), "strategy": strat, "dist": args.dist,
+                   "sigma": args.sigma if args.dist == "lognormal" else None,
+                   "snr_db": snr, "underflow_rate": ur, "overflow_rate": orate}
             if strat == "auto":
                 row["mu"] = mus
             print(json.dumps(row), flush=True)
