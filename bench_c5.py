@@ -95,6 +95,15 @@ def main():
                 B.fp8_grad_allreduce(plan, g, s_g, skip, g8, gs, gsi, sat, mu, comm=c)
 
             res[f"{mode_name}_full"] = timed(full, iters)
+            if mode == B.MODE_P2P:
+                # the same two calls captured in a CUDA graph: one host call per step (the
+                # flag epochs live in device counters, so every replay is a new step)
+                gr = torch.cuda.CUDAGraph()
+                torch.cuda.synchronize()
+                with torch.cuda.graph(gr):
+                    full()
+                res[f"{mode_name}_full_graph"] = timed(gr.replay, iters)
+                del gr
             B.prof_enable(True)                  # a second, instrumented pass for the kernel
             timed(full, iters)
             B.prof_enable(False)
@@ -108,9 +117,16 @@ def main():
         for dt, name, esz in ((torch.bfloat16, "nccl_bf16", 2), (torch.float32, "nccl_f32", 4)):
             x = torch.ones(n, dtype=dt, device="cuda")
             res[name] = timed(lambda: dist.all_reduce(x), iters)
+            if dt == torch.bfloat16:
+                gr = torch.cuda.CUDAGraph()
+                torch.cuda.synchronize()
+                with torch.cuda.graph(gr):
+                    dist.all_reduce(x)
+                res[name + "_graph"] = timed(gr.replay, iters)
+                del gr
             del x
         for impl, us in res.items():
-            payload = n * (2 if impl == "nccl_bf16" else 4 if impl == "nccl_f32" else 1)
+            payload = n * (2 if impl.startswith("nccl_bf16") else 4 if impl == "nccl_f32" else 1)
             algbw = payload / (us * 1e-6) / 1e9
             row = {"config": "C5", "n_gpus": N, "elements": n, "fp8_bytes": n, "impl": impl,
                    "us": us, "algbw_GBs": algbw, "busbw_GBs": algbw * busf,

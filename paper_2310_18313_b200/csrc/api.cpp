@@ -594,13 +594,12 @@ static int check_plan(const fp8lm_plan* p, const fp8lm_comm* comm, const char* w
   return FP8LM_OK;
 }
 
-static P2PArgs p2p_args(const fp8lm_plan* p, uint32_t epoch) {
+static P2PArgs p2p_args(const fp8lm_plan* p) {
   P2PArgs x;
   x.tab = reinterpret_cast<const PeerTable*>(reinterpret_cast<uint8_t*>(p->win_pad) + kPadTable);
   x.pad = p->win_pad;
   x.rank = p->rank;
   x.nranks = p->nranks;
-  x.epoch = epoch;
   return x;
 }
 
@@ -816,7 +815,7 @@ int fp8lm_amax_scale_sync(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, in
   const bool nccl = p->mode == FP8LM_MODE_NCCL;
   if (p->mode == FP8LM_MODE_P2P || p->mode == FP8LM_MODE_ZERO) {
     // A1 amax; its last CTA exchanges the local scales through the peers' pads (Eq. 4)
-    const P2PArgs x = p2p_args(p, ++p->epoch);
+    const P2PArgs x = p2p_args(p);
     CUDA_TRY(launch_amax(p->dev, srcs, nsrc, src_dtype, mu, amax_out, s_g, skip, true, &x, s));
     return FP8LM_OK;
   }
@@ -864,17 +863,17 @@ int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int
     uint8_t* dst[1] = {p->win_send};
     CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, nullptr, s));
     // each owner reduces its whole tensors from every rank's send window
-    CUDA_TRY(launch_reduce_owner(d, p->own->dev, p2p_args(p, p->epoch), g8, s_g, tail, s));
+    CUDA_TRY(launch_reduce_owner(d, p->own->dev, p2p_args(p), g8, s_g, tail, s));
   } else if (p->mode == FP8LM_MODE_P2P) {
     if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "grad_allreduce: mode P2P needs g8 == fp8lm_peer_g8(plan)");
     if (p->g8_bytes <= p->oneshot_max_bytes) {   // small message: one kernel, one handshake
-      CUDA_TRY(launch_oneshot(d, p2p_args(p, p->epoch), srcs[0], src_dtype, g8, s_g, tail, s));
+      CUDA_TRY(launch_oneshot(d, p2p_args(p), srcs[0], src_dtype, g8, s_g, tail, s));
       return FP8LM_OK;
     }
     uint8_t* dst[1] = {p->win_send};
     CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, nullptr, s));
     // A4 + A5 in one kernel over NVLink peer memory (same epoch as this step's amax)
-    CUDA_TRY(launch_reduce_p2p(d, p2p_args(p, p->epoch), g8, s_g, tail, s));
+    CUDA_TRY(launch_reduce_p2p(d, p2p_args(p), g8, s_g, tail, s));
   } else if (p->mode == FP8LM_MODE_SIMULATED) {
     uint8_t* dst[FP8LM_MAX_SIM_RANKS];
     for (int r = 0; r < nsrc; ++r) dst[r] = d.sim_codes + (int64_t)r * p->total;
@@ -938,7 +937,7 @@ int fp8lm_adam_step(fp8lm_plan* p, const uint8_t* g8, const float* g_scale_inv,
     if (!p->p2p_ready) return fail(FP8LM_EINVAL, "adam_step: mode ZERO needs fp8lm_peer_setup first");
     if (p->own->T > 0 && (!g8 || !aligned(g8, 256))) return fail(FP8LM_EINVAL, "adam_step: g8 NULL or misaligned");
     CUDA_TRY(launch_adam(p->own->dev, g8, p->dev.gsinv_own, *m1, *v, *master, *w8, *hp, skip, S(stream)));
-    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p, ++p->epoch_w8),
+    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p),
                              static_cast<const uint8_t*>(w8->data), *w8, S(stream)));
     return FP8LM_OK;
   }
@@ -968,7 +967,7 @@ int fp8lm_adam_step_delayed(fp8lm_plan* p, const uint8_t* g8, const float* g_sca
     if (!p->p2p_ready) return fail(FP8LM_EINVAL, "adam_step_delayed: mode ZERO needs fp8lm_peer_setup first");
     CUDA_TRY(launch_adam_delayed(p->own->dev, g8, p->dev.gsinv_own, *m1, *v, *master, *w8, *hp, skip,
                                  w_hist, hist_slot, S(stream)));
-    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p, ++p->epoch_w8),
+    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p),
                              static_cast<const uint8_t*>(w8->data), *w8, S(stream)));
     return FP8LM_OK;
   }
@@ -1067,7 +1066,7 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
       {
         LaunchPolicy keep = launch_policy();
         if (phase == 1) launch_policy().max_ctas = split_xcap(p);
-        rc = launch_reduce_owner_a1(p->dev, p->own->dev, p2p_args(p, p->epoch), s_g, tail, g8, *m1, *v,
+        rc = launch_reduce_owner_a1(p->dev, p->own->dev, p2p_args(p), s_g, tail, g8, *m1, *v,
                                     *master, *w8, *hp, skip, xs);
         launch_policy() = keep;
         CUDA_TRY((cudaError_t)rc);
@@ -1082,7 +1081,7 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
     // pass 2 on the owned tensors also stores every w8 group into every rank's window
     // (the broadcast overlaps the HBM-bound pass); its last CTA publishes the scalars
     Pass2Ext ext;
-    ext.bcast = p2p_args(p, ++p->epoch_w8);
+    ext.bcast = p2p_args(p);
     ext.own_gpos = p->dev.own_gpos;
     ext.own2full = p->dev.own2full;
     ext.T_full = p->T;
@@ -1104,7 +1103,7 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
     if (!hp || !g_scale || !g_scale_inv || !sat) return fail(FP8LM_EINVAL, "dp_step: NULL argument");
     if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "dp_step: mode P2P needs g8 == fp8lm_peer_g8(plan)");
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
-    P2PArgs x = p2p_args(p, p->epoch);
+    P2PArgs x = p2p_args(p);
     if (phase == 0 && p->g8_bytes <= p->oneshot_max_bytes) {
       // small message: the one-shot exchange leaves the whole reduced set in g8, so both
       // AdamW passes run locally (no pull)
@@ -1231,7 +1230,7 @@ int fp8lm_state_init(fp8lm_plan* p, const float* w0, const fp8lm_stensors* m1,
     if (!p->p2p_ready) return fail(FP8LM_EINVAL, "state_init: mode ZERO needs fp8lm_peer_setup first");
     if (p->own->T > 0 && (!w0 || !aligned(w0, 256))) return fail(FP8LM_EINVAL, "state_init: w0 NULL or misaligned");
     CUDA_TRY(launch_state_init(p->own->dev, w0, *m1, *v, *master, *w8, S(stream)));
-    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p, ++p->epoch_w8),
+    CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, p2p_args(p),
                              static_cast<const uint8_t*>(w8->data), *w8, S(stream)));
     return FP8LM_OK;
   }

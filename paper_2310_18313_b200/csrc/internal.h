@@ -56,14 +56,17 @@ constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2, kCtrFix = 3, kCtrFixGen 
 // per-shard saturation counts).
 constexpr int kMaxPeers = FP8LM_MAX_P2P_RANKS;
 constexpr size_t kPadFlagScale = 0, kPadFlagReady = 64, kPadFlagDone = 128, kPadFlagW8 = 192,
-                 kPadTable = 256, kPadData = 1024;
+                 kPadTable = 256, kPadCtl = 512, kPadData = 1024;
+// kPadCtl: this rank's epoch counters, device-resident so that a captured (CUDA-graph)
+// step advances them on every replay: [0] the step epoch (bumped by k_amax's exchange
+// epilogue, read by the step's later kernels), [1] the w8-broadcast epoch (mode ZERO)
 struct PeerTable {
   uint8_t* send[kMaxPeers];
   uint8_t* g8[kMaxPeers];
   uint32_t* pad[kMaxPeers];
   uint8_t* w8[kMaxPeers];   // mode ZERO: replicated FP8 weight copy (full layout)
 };
-static_assert(kPadTable + sizeof(PeerTable) <= kPadData, "pad layout");
+static_assert(kPadTable + sizeof(PeerTable) <= kPadCtl && kPadCtl + 8 <= kPadData, "pad layout");
 // pad data region: scales [N][T] f32 | sat [N][T] u32 | (ZERO) w8 scalars [3][T] f32 |
 // pass-1 state maxima [N][3T] u32 (fused P2P step)
 inline size_t pad_bytes_for(int N, int T) {
@@ -75,8 +78,12 @@ struct P2PArgs {
   uint32_t* pad;          // this rank's pad
   int rank;
   int nranks;
-  uint32_t epoch;         // step counter: flags hold the epoch of their last signal
 };
+// the step's epoch (flags hold the epoch of their last signal) / the w8 epoch, from the
+// own pad's counters
+__host__ __device__ inline uint32_t* pad_ctl(uint32_t* pad) {
+  return reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pad) + kPadCtl);
+}
 
 // ---------------------------------------------------------------- FP8 SP converter (f4)
 // pad of one rank (bytes): three flag rows (one u32 epoch per source rank), the ranks'
@@ -150,8 +157,6 @@ struct fp8lm_plan {
   uint32_t* win_pad = nullptr;
   size_t pad_bytes = 0;
   std::vector<void*> mapped;
-  uint32_t epoch = 0;
-  uint32_t epoch_w8 = 0;
   bool p2p_ready = false;
   uint8_t* win_w8 = nullptr;
   // single-process loopback of modes P2P / ZERO (fp8lm_peer_setup_loopback): the N ranks

@@ -67,10 +67,11 @@ __device__ __forceinline__ Peers<NR> load_peers(const SpArgs& a) {
 // sys: this CTA wrote memory that peers read (peer stores, the own send window)
 __device__ __forceinline__ bool sp_last_cta(uint32_t* ticket, bool sys) {
   __shared__ int last;
-  if (sys) __threadfence_system();
-  else __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    // one fence per CTA after the barrier: cumulative over every thread's writes
+    if (sys) __threadfence_system();
+    else __threadfence();
     const uint32_t t = atomicAdd(ticket, 1u);
     last = t == gridDim.x - 1;
     if (last) *ticket = 0;

@@ -222,3 +222,64 @@ def test_loopback_split_buckets(B, N, variant):
             if delayed:
                 hists[b] = res["hists"]
         assert not msgs, "\n".join(msgs[:10])
+
+
+@pytest.mark.parametrize("N", [2, 4])
+@pytest.mark.parametrize("oneshot", [True, False], ids=["oneshot", "rsag"])
+def test_loopback_graph_replay_allreduce(B, N, oneshot):
+    """The P2P exchange captured in a CUDA graph (one per rank, on its stream) and
+    replayed: fp8lm_amax_scale_sync + fp8lm_grad_allreduce read their flag epochs from the
+    pads' device counters (kPadCtl), so every replay is a new step.  Each replay's inputs
+    are copied into the captured gradient buffer; results vs the N-rank oracle every step."""
+    import synth
+    from oracle import pipeline as OP
+    plans = [B.Plan(RAGGED, mode=B.MODE_P2P, nranks=N, rank=r) for r in range(N)]
+    for p_ in plans:
+        p_.set_oneshot(1 << 40 if oneshot else 0)
+    B.peer_setup_loopback(plans)
+    plan = plans[0]
+    T = plan.T
+    bufs = []
+    for r in range(N):
+        bufs.append(dict(g=plan.flat(torch.float32), g8=plans[r].peer_g8(),
+                         mu=torch.ones(T, device="cuda"), amax=torch.zeros(T, device="cuda"),
+                         s_g=torch.zeros(T, device="cuda"), skip=torch.zeros(1, dtype=torch.int32, device="cuda"),
+                         gs=torch.zeros(T, device="cuda"), gsi=torch.zeros(T, device="cuda"),
+                         sat=torch.zeros(T, dtype=torch.int32, device="cuda")))
+    streams = [torch.cuda.Stream() for _ in range(N)]
+    torch.cuda.synchronize()
+
+    def call(r):
+        b = bufs[r]
+        B.amax_scale_sync(plans[r], b["g"], b["mu"], b["amax"], b["s_g"], b["skip"])
+        B.fp8_grad_allreduce(plans[r], b["g"], b["s_g"], b["skip"], b["g8"], b["gs"], b["gsi"], b["sat"], b["mu"])
+
+    graphs = [torch.cuda.CUDAGraph() for _ in range(N)]
+    # capture: the captured launches do not run; the device counters advance only on replay
+    for r in range(N):
+        with torch.cuda.graph(graphs[r], stream=streams[r]):
+            call(r)
+    torch.cuda.synchronize()
+    mus = [F32(1.0)] * T
+    for step in range(1, 4):
+        grads = R.make_grads(plan, N, step, "cuda", specials=lambda f, r: _huge(f, r, step))
+        for r in range(N):
+            bufs[r]["g"].copy_(grads[r])
+        torch.cuda.synchronize()
+        for r in range(N):
+            with torch.cuda.stream(streams[r]):
+                graphs[r].replay()
+        torch.cuda.synchronize()
+        per_rank = [[R.to_np_f32(g[plan.offsets[t]: plan.offsets[t] + plan.numels[t]]) for t in range(T)]
+                    for g in grads]
+        for t in range(T):
+            ref = OP.allreduce_tensor([per_rank[r][t] for r in range(N)], mus[t])
+            for r in range(N):
+                b = bufs[r]
+                sl = slice(plan.offsets[t], plan.offsets[t] + plan.numels[t])
+                # fp8lm_grad_allreduce leaves the whole reduced set in every rank's g8
+                assert np.array_equal(b["g8"].cpu().numpy()[sl], ref["codes"]), (step, t, r)
+                assert F32(b["s_g"][t].item()) == ref["s_g"] and int(b["sat"][t].item()) == ref["sat"], (step, t, r)
+            mus[t] = OP.mu_update(mus[t], ref["sat"], ref["n"], False)
+            assert F32(bufs[0]["mu"][t].item()) == mus[t], (step, t)
+    assert B.peer_timeout_report()[0] == 0
