@@ -3,10 +3,10 @@
 NCCL bf16, under torchrun on N GPUs of one box.
 
 For every FP8 payload size n (bytes = elements) it times, max over ranks, CUDA events:
-  p2p_full  — amax_scale_sync + fp8_grad_allreduce in mode P2P from an fp32 gradient
-              (amax, MIN of scales through peer pads, then up to 1 MiB the one-shot
-              exchange kernel, above it quantize + the fused peer-memory reduce-scatter +
-              rank-order reduce + all-gather)
+  p2p_full  — fp8lm_allreduce_jit (= amax_scale_sync + fp8_grad_allreduce) in mode P2P
+              from an fp32 gradient: up to 1 MiB ONE kernel (amax, MIN of the scales
+              through the peer pads, the one-shot exchange), above it amax + quantize + the
+              fused peer-memory reduce-scatter + rank-order reduce + all-gather
   p2p_rsag_full — up to 1 MiB: the same with the one-shot path off (quantize + RS + AG)
   p2p_xchg  — the fused exchange kernel alone (k_reduce_p2p, library launch tracing)
   nccl_full — the same arithmetic with NCCL transport (mode NCCL)
@@ -90,9 +90,8 @@ def main():
             gsi = torch.zeros(1, device="cuda")
             sat = torch.zeros(1, dtype=torch.int32, device="cuda")
 
-            def full():
-                B.amax_scale_sync(plan, g, mu, amax, s_g, skip, comm=c)
-                B.fp8_grad_allreduce(plan, g, s_g, skip, g8, gs, gsi, sat, mu, comm=c)
+            def full():       # A1-A5: fp8lm_allreduce_jit (P2P small plans: one kernel)
+                B.allreduce_jit(plan, g, mu, amax, s_g, skip, g8, gs, gsi, sat, comm=c)
 
             res[f"{mode_name}_full"] = timed(full, iters)
             if mode == B.MODE_P2P:

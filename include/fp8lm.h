@@ -269,6 +269,15 @@ int fp8lm_grad_allreduce(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
                          uint8_t* g8, float* g_scale, float* g_scale_inv, uint32_t* sat,
                          float* mu, void* stream);
 
+/* (2) + (3) in one call: fp8lm_amax_scale_sync then fp8lm_grad_allreduce, same
+ * arguments and results.  Mode P2P with a small plan (fp8lm_plan_set_oneshot): ONE kernel
+ * — amax, the Eq. 4 MIN through the pads, the one-shot exchange — one launch and two
+ * cross-rank handshakes per step (config C5's small messages).  Other modes / sizes: the
+ * two calls. */
+int fp8lm_allreduce_jit(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
+                        float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                        float* g_scale, float* g_scale_inv, uint32_t* sat, void* stream);
+
 /* --------------------------------- (4) fp8_adam_step: §2.2, A6 + A7 */
 /* Precision-decoupled AdamW on every tensor of the plan, JIT state scaling (R18):
  *   g  = fl(decode(g8) * g_scale_inv[t])        (dequantize, A6)

@@ -9,7 +9,7 @@ from ._binding import (  # noqa: F401
     ALIGN_ELEMS, BF16, E4M3, E5M2, F16, F32, MODE_LOCAL, MODE_NCCL, MODE_P2P, MODE_SIMULATED, MODE_ZERO,
     CompactLayout,
     AdamHP, Comm, FP8DataParallel, FP8LMError, OptimizerState, Plan, STensorSet, adam_hp,
-    amax_scale_sync, fp8_adam_step, fp8_adam_step_delayed, fp8_dequantize, fp8_grad_allreduce, fp8_quantize,
+    allreduce_jit, amax_scale_sync, fp8_adam_step, fp8_adam_step_delayed, fp8_dequantize, fp8_grad_allreduce, fp8_quantize,
     has_nccl, lib, LIB_PATH, prof_enable, prof_read, state_init, version, zero_plan,
     STRATEGIES, allreduce_strategy, commstats_buffer, commstats_metrics, commstats_read, SPConverter,
     peer_setup_loopback, peer_timeout_report, set_peer_timeout, BucketedDP, bucket_split,

@@ -88,6 +88,7 @@ _sig("fp8lm_quantize", C.c_int, _p, _i32, _i64, _i32, _p, _p, _p, _p, _i32, _p, 
 _sig("fp8lm_dequantize", C.c_int, _p, _i32, _i64, _p, _p, _p)
 _sig("fp8lm_amax_scale_sync", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p)
 _sig("fp8lm_grad_allreduce", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p)
+_sig("fp8lm_allreduce_jit", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p)
 _sig("fp8lm_adam_step", C.c_int, _p, _p, _p, C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(STensors), C.POINTER(STensors), C.POINTER(AdamHP), _p, _p)
 _sig("fp8lm_prof_enable", C.c_int, C.c_int)
@@ -576,6 +577,18 @@ def fp8_grad_allreduce(plan: Plan, grads, s_g: torch.Tensor, skip: torch.Tensor,
                                     _ptr(skip), _ptr(g8), _ptr(g_scale), _ptr(g_scale_inv),
                                     _ptr(sat), _ptr(mu), _stream(stream)),
            "fp8lm_grad_allreduce")
+    del keep
+
+
+def allreduce_jit(plan: Plan, grads, mu: torch.Tensor, amax_out: torch.Tensor, s_g: torch.Tensor,
+                  skip: torch.Tensor, g8: torch.Tensor, g_scale: torch.Tensor, g_scale_inv: torch.Tensor,
+                  sat: torch.Tensor, comm: Comm = None, stream=None):
+    """fp8lm_allreduce_jit: amax_scale_sync + fp8_grad_allreduce in one call (mode P2P,
+    small plans: one kernel)."""
+    g, dt, keep = _grads_arg(plan, grads)
+    _check(lib.fp8lm_allreduce_jit(plan.handle, comm.handle if comm else None, g, dt, _ptr(mu), _ptr(amax_out),
+                                   _ptr(s_g), _ptr(skip), _ptr(g8), _ptr(g_scale), _ptr(g_scale_inv), _ptr(sat),
+                                   _stream(stream)), "fp8lm_allreduce_jit")
     del keep
 
 

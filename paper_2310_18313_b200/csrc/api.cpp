@@ -908,6 +908,29 @@ int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int
   return FP8LM_OK;
 }
 
+// ---------------------------------------------------------------- (2) + (3) in one call
+int fp8lm_allreduce_jit(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype, float* mu,
+                        float* amax_out, float* s_g, int32_t* skip, uint8_t* g8, float* g_scale,
+                        float* g_scale_inv, uint32_t* sat, void* stream) {
+  const LaunchScope ls_(p);
+  int rc = check_plan(p, comm, "allreduce_jit");
+  if (rc) return rc;
+  if (p->mode == FP8LM_MODE_P2P && p->T > 0 && p->g8_bytes <= p->oneshot_max_bytes) {
+    const void* srcs[1];
+    int nsrc = 0;
+    if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "allreduce_jit"))) return rc;
+    if (!mu || !amax_out || !s_g || !skip || !g_scale || !g_scale_inv || !sat)
+      return fail(FP8LM_EINVAL, "allreduce_jit: NULL output");
+    if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "allreduce_jit: mode P2P needs g8 == fp8lm_peer_g8(plan)");
+    const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
+    CUDA_TRY(launch_oneshot_full(p->dev, p2p_args(p), srcs[0], src_dtype, mu, amax_out, s_g, skip, g8, tail,
+                                 S(stream)));
+    return FP8LM_OK;
+  }
+  if ((rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream))) return rc;
+  return fp8lm_grad_allreduce(p, comm, grads, src_dtype, s_g, skip, g8, g_scale, g_scale_inv, sat, mu, stream);
+}
+
 // ---------------------------------------------------------------- (4) fp8_adam_step
 static int check_stensors(const fp8lm_plan* p, const fp8lm_stensors* x, const char* name,
                           const char* who) {
@@ -1026,9 +1049,27 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
   const LaunchScope ls_(p);   // loopback plans: capped grids
   const CapScope hcap_(phase ? FP8LM_SPLIT_HCAP * num_sms() : 0);
   int rc;
+  const bool delayed = w_hist != nullptr;
+  if (phase == 0 && p && p->mode == FP8LM_MODE_P2P && p->T > 0 && p->g8_bytes <= p->oneshot_max_bytes) {
+    // small message: A1-A5 in one kernel (the one-shot exchange leaves the whole reduced
+    // set in g8), then both AdamW passes locally
+    if ((rc = check_stensors(p, m1, "m1", "dp_step")) || (rc = check_stensors(p, v, "v", "dp_step")) ||
+        (rc = check_stensors(p, master, "master", "dp_step")) || (rc = check_stensors(p, w8, "w8", "dp_step")))
+      return rc;
+    if (!hp) return fail(FP8LM_EINVAL, "dp_step: NULL hp");
+    if (delayed && (hist_slot < 0 || hist_slot >= 16)) return fail(FP8LM_EINVAL, "dp_step: hist_slot not in [0, 16)");
+    if ((rc = fp8lm_allreduce_jit(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, g8, g_scale, g_scale_inv,
+                                  sat, stream)))
+      return rc;
+    if (delayed)
+      CUDA_TRY(launch_adam_delayed(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, w_hist,
+                                   hist_slot, S(stream)));
+    else
+      CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream)));
+    return FP8LM_OK;
+  }
   if (phase != 2 && (rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream)))
     return rc;
-  const bool delayed = w_hist != nullptr;
   if (delayed && (hist_slot < 0 || hist_slot >= 16)) return fail(FP8LM_EINVAL, "dp_step: hist_slot not in [0, 16)");
   // SIMULATED with 2..4 ranks (config C1): quantize + rank-order reduce + Adam pass 1 in one
   // kernel, like LOCAL; more ranks (tests up to 16) and delayed scaling take the three calls
@@ -1104,20 +1145,6 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
     if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "dp_step: mode P2P needs g8 == fp8lm_peer_g8(plan)");
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
     P2PArgs x = p2p_args(p);
-    if (phase == 0 && p->g8_bytes <= p->oneshot_max_bytes) {
-      // small message: the one-shot exchange leaves the whole reduced set in g8, so both
-      // AdamW passes run locally (no pull)
-      const void* srcs[1];
-      int nsrc = 0;
-      if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
-      CUDA_TRY(launch_oneshot(p->dev, x, srcs[0], src_dtype, g8, s_g, tail, S(stream)));
-      if (delayed)
-        CUDA_TRY(launch_adam_delayed(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, w_hist,
-                                     hist_slot, S(stream)));
-      else
-        CUDA_TRY(launch_adam(p->dev, g8, g_scale_inv, *m1, *v, *master, *w8, *hp, skip, S(stream)));
-      return FP8LM_OK;
-    }
     if (phase != 2) {
       const void* srcs[1];
       int nsrc = 0;

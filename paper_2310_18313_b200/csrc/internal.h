@@ -47,7 +47,7 @@ struct DevPlan {
 };
 
 constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2, kCtrFix = 3, kCtrFixGen = 4, kCtrOneshot = 5,
-              kCtrWords = 8;
+              kCtrPhase = 6 /* k_oneshot_full's phase word: the last released epoch */, kCtrWords = 8;
 
 // ---------------------------------------------------------------- mode P2P windows
 // Signal / exchange pad of one rank (bytes): three flag arrays (one u32 epoch slot per
@@ -209,6 +209,10 @@ cudaError_t launch_reduce_p2p(const DevPlan& p, const P2PArgs& x, uint8_t* g8, c
 // reduces the WHOLE tensor set from every rank (one kernel, one cross-rank handshake)
 cudaError_t launch_oneshot(const DevPlan& p, const P2PArgs& x, const void* src, int src_dtype,
                            uint8_t* g8, const float* s_g, const TailArgs& tail, cudaStream_t s);
+// A1-A5 of a small plan in one kernel: amax, MIN through the pads, then the one-shot body
+cudaError_t launch_oneshot_full(const DevPlan& p, const P2PArgs& x, const void* src, int src_dtype,
+                                const float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                                const TailArgs& tail, cudaStream_t s);
 // mode ZERO: owner reduce over the compact sub-plan `o` (items), tails on the full plan `p`
 cudaError_t launch_reduce_owner(const DevPlan& p, const DevPlan& o, const P2PArgs& x, uint8_t* g8,
                                 const float* s_g, const TailArgs& tail, cudaStream_t s);

@@ -225,8 +225,9 @@ def test_loopback_split_buckets(B, N, variant):
 
 
 @pytest.mark.parametrize("N", [2, 4])
-@pytest.mark.parametrize("oneshot", [True, False], ids=["oneshot", "rsag"])
-def test_loopback_graph_replay_allreduce(B, N, oneshot):
+@pytest.mark.parametrize("oneshot,jit", [(True, False), (False, False), (True, True), (False, True)],
+                         ids=["oneshot", "rsag", "oneshot_jit", "rsag_jit"])
+def test_loopback_graph_replay_allreduce(B, N, oneshot, jit):
     """The P2P exchange captured in a CUDA graph (one per rank, on its stream) and
     replayed: fp8lm_amax_scale_sync + fp8lm_grad_allreduce read their flag epochs from the
     pads' device counters (kPadCtl), so every replay is a new step.  Each replay's inputs
@@ -251,6 +252,10 @@ def test_loopback_graph_replay_allreduce(B, N, oneshot):
 
     def call(r):
         b = bufs[r]
+        if jit:      # fp8lm_allreduce_jit: one kernel for a small plan (k_oneshot_full)
+            B.allreduce_jit(plans[r], b["g"], b["mu"], b["amax"], b["s_g"], b["skip"], b["g8"], b["gs"], b["gsi"],
+                            b["sat"])
+            return
         B.amax_scale_sync(plans[r], b["g"], b["mu"], b["amax"], b["s_g"], b["skip"])
         B.fp8_grad_allreduce(plans[r], b["g"], b["s_g"], b["skip"], b["g8"], b["gs"], b["gsi"], b["sat"], b["mu"])
 
