@@ -86,8 +86,11 @@ __device__ __forceinline__ bool sp_last_cta(uint32_t* ticket, bool sys) {
 
 template <int NR>
 __device__ __forceinline__ void release_all(const Peers<NR>& P, size_t off, int rank, uint32_t e) {
+  // one system fence, then relaxed flag stores (a release pattern per flag): N sequential
+  // st.release.sys would cost N x ~1.5 us in this one thread
+  __threadfence_system();
 #pragma unroll
-  for (int q = 0; q < NR; ++q) st_release_sys(sp_flags(P.pad[q], off) + rank, e);
+  for (int q = 0; q < NR; ++q) st_relaxed_sys(sp_flags(P.pad[q], off) + rank, e);
 }
 
 __device__ __forceinline__ int64_t cta_lo(int64_t n) { return n * blockIdx.x / gridDim.x; }
@@ -195,7 +198,6 @@ __device__ __forceinline__ void phase_scale(const T* __restrict__ x, int64_t n, 
 #pragma unroll
     for (int q = 0; q < NR; ++q)
       reinterpret_cast<volatile float*>(sp_flags(P.pad[q], kSpPadScales))[a.rank] = sr;
-    __threadfence_system();
     release_all<NR>(P, kSpPadFlagScale, a.rank, a.epoch);
     wait_epoch(sp_flags(a.pad, kSpPadFlagScale), NR, a.epoch);
     // Eq. 4: the MIN of the ranks' scales; every rank zero / tiny -> 1
@@ -251,7 +253,8 @@ __device__ __forceinline__ void phase_quant(const T* __restrict__ x, int64_t n, 
     if (PUSH) own_recv[dst_off + i] = c;
     else own_send[i] = c;
   }
-  grid_phase(a, kSpScrTicketB, kSpScrFlag2, true, [&] { release_all<NR>(P, kSpPadFlagData, a.rank, a.epoch); });
+  // the codes are local (own window): a gpu-scope ticket, release_all's fence.sys covers them
+  grid_phase(a, kSpScrTicketB, kSpScrFlag2, false, [&] { release_all<NR>(P, kSpPadFlagData, a.rank, a.epoch); });
   if (threadIdx.x == 0) wait_epoch(sp_flags(a.pad, kSpPadFlagData), NR, a.epoch);
   __syncthreads();
 }
@@ -305,7 +308,6 @@ __global__ void __launch_bounds__(kSpT) k_sp_allgather(const T* __restrict__ x, 
     }
   }
   if (sp_last_cta(a.scratch + kSpScrTicketC, false) && threadIdx.x == 0) {
-    __threadfence_system();
     release_all<NR>(P, kSpPadFlagDone, a.rank, a.epoch);
   }
 }
@@ -351,7 +353,6 @@ __global__ void __launch_bounds__(kSpT) k_sp_reduce_scatter(const T* __restrict_
     Out<O>::put(out, i, __fmul_rn(S, sinv));
   }
   if (sp_last_cta(a.scratch + kSpScrTicketC, false) && threadIdx.x == 0) {
-    __threadfence_system();
     release_all<NR>(P, kSpPadFlagDone, a.rank, a.epoch);
   }
 }
