@@ -533,7 +533,19 @@ def main():
     # launches per step of the dominant kernel (buckets: one per bucket): bytes per launch
     # are the per-step bytes over that count
     lps = max(1.0, ours[dom]["launches"] / args.steps) if dom else 1.0
-    if zero and dom == "adam_pass2" and N > 1:
+    if nb > 1:
+        # split step: the exchange kernels of one bucket run beside the HBM passes of the
+        # others, so a kernel's own event-bracketed time includes the time it shared the
+        # GPU; the meaningful roofline is the whole step's (HBM-bound: every rank streams
+        # its states and gradient once or twice, the NVLink traffic rides beside it)
+        achieved = bytes_rank / (ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": f"whole step ({nb} buckets, overlapped kernels)",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_kind": hbm_kind, "traffic": None, "alg_bytes_per_launch": bytes_rank,
+                "avg_launch_ms": ms, "share_of_step": 1.0,
+                "note": "per rank; algorithmic bytes of SURVEY 8(d) (pass 1 counted whole although "
+                        "each rank runs 1/N of it)"}
+    elif zero and dom == "adam_pass2" and N > 1:
         # ZeRO dp_step: the owner's pass 2 also stores every w8 code into the N-1 peers'
         # windows, (N-1) bytes per owned parameter out of this GPU over NVLink, under its
         # own 12 B/param of HBM traffic; the link is the bound (the HBM fraction rides along)
