@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--state-scaling", default="jit", choices=["jit", "delayed"],
                     help="optimizer-state scales: just-in-time (two AdamW passes, R19) or "
                          "delayed from a 16-step amax history (one pass, R25-R27)")
+    ap.add_argument("--graph", action="store_true",
+                    help="run the step as a CUDA graph (fp8lm_dp_step_graphed; single-plan steps)")
     ap.add_argument("--worst-case", action="store_true",
                     help="data-dependent worst case: lr 0.05 moves the largest weights far beyond the "
                          "amax(w') screen's margin, so pass 2's prologue recomputes pass 1 exactly for "
@@ -458,7 +460,8 @@ def main():
         dp = B.BucketedDP(plans, w0s, comm=comm, lr=args.lr, state_scaling=args.state_scaling,
                           lag=args.bucket_lag)
     else:
-        dp = B.FP8DataParallel(plans[0], w0s[0], comm=comm, lr=args.lr, state_scaling=args.state_scaling)
+        dp = B.FP8DataParallel(plans[0], w0s[0], comm=comm, lr=args.lr, state_scaling=args.state_scaling,
+                               graphed=args.graph)
     dps = dp.dps if nb > 1 else [dp]
     del w0s
     torch.cuda.synchronize()
@@ -506,6 +509,8 @@ def main():
 
     barrier(world)
     torch.cuda.synchronize()
+    for d_ in dps:           # per-kernel tracing needs the launches: the same kernels, eagerly
+        d_.graphed = False
     B.prof_enable(True)
     ev0.record(stream)
     for _ in range(args.steps):
@@ -672,6 +677,7 @@ def main():
             "config": {"workload": WORKLOAD[args.config] + (", ZeRO owner mode (Alg. 1)" if zero else ""),
                        "tensors": len(numels), "params": params, "grad_dtype": args.dtype,
                        "buckets": nb, "bucket_lag": args.bucket_lag, "lr": args.lr,
+                       "cuda_graph": bool(args.graph and nb == 1),
                        "case": "worst (amax(w') screen fallback)" if args.worst_case else "typical",
                        "alg_bytes_per_param_per_rank": bytes_rank / params,
                        "parallelism": f"dp{N}" if N > 1 else (f"{sim} simulated ranks" if sim else "single"), "state_scaling": args.state_scaling,

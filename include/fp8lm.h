@@ -358,6 +358,23 @@ int fp8lm_dp_step_split(fp8lm_plan* plan, int32_t phase, const void* grads, int3
                         const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
                         int32_t hist_slot, void* stream);
 
+/* fp8lm_dp_step as a CUDA graph: same arguments and results.  The first call with a set
+ * of buffers runs eagerly; the second captures the step on `stream`
+ * (cudaStreamCaptureModeThreadLocal), instantiates and launches the graph; later calls
+ * patch the step's scalars (hp, hist_slot) into the graph's AdamW kernel nodes and
+ * relaunch it — one host call and no per-kernel launch work per step.  Every other
+ * per-step value is device-resident (μ, scales, the P2P / ZERO flag epochs in the pads).
+ * A graph belongs to one set of pointers (grads, outputs, states, w_hist, comm, stream)
+ * and dtype; the plan keeps the 4 most recently used (callers that rotate gradient
+ * buffers).  Mode NCCL: plain fp8lm_dp_step.  The caller must not capture `stream`
+ * itself around this call. */
+int fp8lm_dp_step_graphed(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
+                          float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                          float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
+                          const fp8lm_stensors* v, const fp8lm_stensors* master,
+                          const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
+                          int32_t hist_slot, void* stream);
+
 /* Initial optimizer state: m1, v = zero codes with scale 1,
  * amax 0; master / w8 JIT-encoded from the FP32 flat weights w0 (plan layout).
  * Mode ZERO: w0 and the states are COMPACT (owned tensors); the replicated w8 copy is

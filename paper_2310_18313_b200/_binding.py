@@ -99,6 +99,9 @@ _sig("fp8lm_selftest_fastmath", C.c_int, _u64, _u64, C.POINTER(_u64))
 _sig("fp8lm_dp_step", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
      C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(AdamHP), _p, _i32, _p)
+_sig("fp8lm_dp_step_graphed", C.c_int, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
+     C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors),
+     C.POINTER(AdamHP), _p, _i32, _p)
 _sig("fp8lm_dp_step_split", C.c_int, _p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
      C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors), C.POINTER(STensors),
      C.POINTER(AdamHP), _p, _i32, _p)
@@ -625,8 +628,11 @@ class FP8DataParallel:
 
     def __init__(self, plan: Plan, w0_flat: torch.Tensor, comm: Comm = None, lr: float = 3e-4,
                  betas=(0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.1,
-                 fused: bool = True, state_scaling: str = "jit"):
+                 fused: bool = True, state_scaling: str = "jit", graphed: bool = False):
+        """graphed: fp8lm_dp_step_graphed — the step as a CUDA graph (captured on the
+        second call with the same buffers, then replayed with the step's scalars patched)."""
         self.fused = fused
+        self.graphed = graphed
         assert state_scaling in ("jit", "delayed")
         self.delayed = state_scaling == "delayed"
         self.plan, self.comm = plan, comm
@@ -672,12 +678,13 @@ class FP8DataParallel:
             g, dt, keep = _grads_arg(self.plan, grads)
             st = self.state
             m1, v, w, w8 = st.m1.c(), st.v.c(), st.master.c(), st.w8.c()
-            _check(lib.fp8lm_dp_step(self.plan.handle, self.comm.handle if self.comm else None, g, dt,
-                                     _ptr(self.mu), _ptr(self.amax), _ptr(self.s_g), _ptr(self.skip),
-                                     _ptr(self.g8), _ptr(self.g_scale), _ptr(self.g_scale_inv),
-                                     _ptr(self.sat), C.byref(m1), C.byref(v), C.byref(w),
-                                     C.byref(w8), C.byref(hp), _ptr(self.w_hist), (self.t - 1) % 16,
-                                     _stream(stream)), "fp8lm_dp_step")
+            fn = lib.fp8lm_dp_step_graphed if self.graphed else lib.fp8lm_dp_step
+            _check(fn(self.plan.handle, self.comm.handle if self.comm else None, g, dt,
+                      _ptr(self.mu), _ptr(self.amax), _ptr(self.s_g), _ptr(self.skip),
+                      _ptr(self.g8), _ptr(self.g_scale), _ptr(self.g_scale_inv),
+                      _ptr(self.sat), C.byref(m1), C.byref(v), C.byref(w),
+                      C.byref(w8), C.byref(hp), _ptr(self.w_hist), (self.t - 1) % 16,
+                      _stream(stream)), "fp8lm_dp_step")
             del keep
             return
         self._three_calls(grads, hp, stream)

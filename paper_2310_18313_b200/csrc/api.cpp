@@ -318,7 +318,13 @@ int fp8lm_plan_destroy(fp8lm_plan* plan) {
   if (plan->win_g8) cudaFree(plan->win_g8);
   if (plan->win_pad) cudaFree(plan->win_pad);
   if (plan->win_w8) cudaFree(plan->win_w8);
+  for (auto& g : plan->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    if (g.log) adam_log_free(g.log);
+  }
   if (plan->xs) cudaStreamDestroy(plan->xs);
+  if (plan->gs) cudaStreamDestroy(plan->gs);
   if (plan->ev_q) cudaEventDestroy(plan->ev_q);
   if (plan->ev_x) cudaEventDestroy(plan->ev_x);
   if (plan->own) fp8lm_plan_destroy(plan->own);
@@ -1241,6 +1247,79 @@ int fp8lm_dp_step_split(fp8lm_plan* p, int32_t phase, const void* grads, int32_t
                     m1, v, master, w8, hp, w_hist, hist_slot, stream, phase);
   if (!rc) p->split_open = phase == 1;
   return rc;
+}
+
+int fp8lm_dp_step_graphed(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
+                          float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                          float* g_scale, float* g_scale_inv, uint32_t* sat, const fp8lm_stensors* m1,
+                          const fp8lm_stensors* v, const fp8lm_stensors* master,
+                          const fp8lm_stensors* w8, const fp8lm_adam_hp* hp, float* w_hist,
+                          int32_t hist_slot, void* stream) {
+  if (!p) return fail(FP8LM_EINVAL, "dp_step_graphed: plan is NULL");
+  auto eager = [&] {
+    return dp_step_impl(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, g8, g_scale, g_scale_inv, sat, m1, v,
+                        master, w8, hp, w_hist, hist_slot, stream, 0);
+  };
+  if (p->mode == FP8LM_MODE_NCCL || !hp || !m1 || !v || !master || !w8) return eager();
+  // the graph is valid for one set of buffers: every pointer argument, the dtype, the
+  // state scaling and the stream
+  std::vector<uintptr_t> key = {(uintptr_t)comm, (uintptr_t)src_dtype, (uintptr_t)mu, (uintptr_t)amax_out,
+                                (uintptr_t)s_g, (uintptr_t)skip, (uintptr_t)g8, (uintptr_t)g_scale,
+                                (uintptr_t)g_scale_inv, (uintptr_t)sat, (uintptr_t)w_hist, (uintptr_t)stream};
+  if (p->mode == FP8LM_MODE_SIMULATED) {
+    const void* const* arr = static_cast<const void* const*>(grads);
+    for (int r = 0; arr && r < p->nranks; ++r) key.push_back((uintptr_t)arr[r]);
+  } else {
+    key.push_back((uintptr_t)grads);
+  }
+  for (const fp8lm_stensors* st : {m1, v, master, w8}) {
+    key.push_back((uintptr_t)st->data); key.push_back((uintptr_t)st->scale);
+    key.push_back((uintptr_t)st->scale_inv); key.push_back((uintptr_t)st->amax);
+  }
+  cudaStream_t s = S(stream);
+  constexpr size_t kMaxGraphs = 4;
+  fp8lm_plan::GraphEntry* ge = nullptr;
+  for (auto& g : p->graphs)
+    if (g.key == key) ge = &g;
+  if (!ge) {                          // new buffers: a new entry (the least recently used goes)
+    if (p->graphs.size() >= kMaxGraphs) {
+      auto lru = std::min_element(p->graphs.begin(), p->graphs.end(),
+                                  [](const auto& x, const auto& y) { return x.used < y.used; });
+      if (lru->exec) cudaGraphExecDestroy(lru->exec);
+      if (lru->graph) cudaGraphDestroy(lru->graph);
+      if (lru->log) adam_log_free(lru->log);
+      p->graphs.erase(lru);
+    }
+    p->graphs.emplace_back();
+    ge = &p->graphs.back();
+    ge->key = key;
+  }
+  ge->used = ++p->graph_clock;
+  if (!ge->exec && ge->seen++ == 0) return eager();   // first call: modules load, caches fill
+  if (!ge->exec) {                    // second call: capture this step, then launch it
+    if (ge->log) adam_log_free(ge->log);
+    ge->log = adam_log_new();
+    // capture on a plan-owned stream (the caller's may be the legacy default stream,
+    // which cannot be captured); the graph is then launched on the caller's stream
+    if (!p->gs) CUDA_TRY(cudaStreamCreateWithFlags(&p->gs, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamBeginCapture(p->gs, cudaStreamCaptureModeThreadLocal));
+    adam_log_activate(ge->log);
+    const int rc = dp_step_impl(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, g8, g_scale, g_scale_inv, sat,
+                                m1, v, master, w8, hp, w_hist, hist_slot, p->gs, 0);
+    adam_log_activate(nullptr);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(p->gs, &g);
+    if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+    CUDA_TRY(ce);
+    ge->graph = g;
+    CUDA_TRY(cudaGraphInstantiate(&ge->exec, g, 0));
+    CUDA_TRY(cudaGraphLaunch(ge->exec, s));
+    return FP8LM_OK;
+  }
+  // replay: patch this step's scalars into the AdamW nodes, launch
+  CUDA_TRY(adam_log_update(ge->log, ge->exec, *hp, hist_slot));
+  CUDA_TRY(cudaGraphLaunch(ge->exec, s));
+  return FP8LM_OK;
 }
 
 int fp8lm_state_init(fp8lm_plan* p, const float* w0, const fp8lm_stensors* m1,

@@ -121,6 +121,8 @@ struct Pass2Ext {
   int T_full = 0;
 };
 
+struct GraphAdamLog;   // kernels.cu: the captured AdamArgs launches of a graphed step
+
 // outputs of the Eq. 6 / mu tail of fp8lm_grad_allreduce
 struct TailArgs {
   int nranks;
@@ -171,6 +173,19 @@ struct fp8lm_plan {
   cudaStream_t xs = nullptr;
   cudaEvent_t ev_q = nullptr, ev_x = nullptr;
   bool split_open = false;
+  // fp8lm_dp_step_graphed: captured steps, one per set of pointer arguments (and dtype,
+  // state scaling, stream) — a few, for callers that rotate gradient buffers
+  struct GraphEntry {
+    std::vector<uintptr_t> key;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    fp8lm::GraphAdamLog* log = nullptr;
+    int seen = 0;                    // calls with this key (the 2nd one captures)
+    uint64_t used = 0;               // LRU stamp
+  };
+  std::vector<GraphEntry> graphs;
+  uint64_t graph_clock = 0;
+  cudaStream_t gs = nullptr;         // the capture stream
   // mode ZERO: Alg. 1 owners, the owned tensors and the compact sub-plan over them
   std::vector<int32_t> owner, own2full;
   std::vector<int64_t> own_gpos, full2own_off;
@@ -287,6 +302,15 @@ struct LaunchScope {
   explicit LaunchScope(const fp8lm_plan* p);
   ~LaunchScope() { launch_policy() = saved; }
 };
+
+// CUDA-graph capture of a step (kernels.cu): the log of the captured AdamArgs launches
+struct GraphAdamLog;
+GraphAdamLog* adam_log_new();
+void adam_log_free(GraphAdamLog* l);
+void adam_log_activate(GraphAdamLog* l);      // thread-local; nullptr = off
+size_t adam_log_size(const GraphAdamLog* l);
+cudaError_t adam_log_update(const GraphAdamLog* l, cudaGraphExec_t exec, const fp8lm_adam_hp& hp,
+                            int hist_slot);
 
 // the peer-wait watchdog of every compilation unit that spins on peer flags (device.cuh)
 cudaError_t wait_watchdog_set_kernels(unsigned long long ns, uint32_t* report);

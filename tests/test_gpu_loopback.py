@@ -48,7 +48,7 @@ def B():
 
 
 def run_loopback(B, numels, mode, N, steps, fused=True, delayed=False, lr=3e-4, sub=None,
-                 specials=None, oneshot=False):
+                 specials=None, oneshot=False, graphed=False):
     """oneshot: mode P2P's small-message exchange (fp8lm_plan_set_oneshot); off by
     default so that these small sets take the reduce-scatter / all-gather kernels."""
     import synth
@@ -67,7 +67,8 @@ def run_loopback(B, numels, mode, N, steps, fused=True, delayed=False, lr=3e-4, 
     for r in range(N):
         with torch.cuda.stream(streams[r]):
             dps.append(B.FP8DataParallel(plans[r], w0, lr=lr, fused=fused,
-                                         state_scaling="delayed" if delayed else "jit"))
+                                         state_scaling="delayed" if delayed else "jit", graphed=graphed))
+    gbufs = None
     torch.cuda.synchronize()
     plan = plans[0]
     sub = list(range(plan.T)) if sub is None else list(sub)
@@ -79,10 +80,16 @@ def run_loopback(B, numels, mode, N, steps, fused=True, delayed=False, lr=3e-4, 
         grads = R.make_grads(plan, N, step, "cuda",
                              specials=(lambda f, r: specials(f, r, step)) if specials else None)
         torch.cuda.synchronize()
+        if graphed:      # the captured steps read the same buffers every step
+            if gbufs is None:
+                gbufs = [g.clone() for g in grads]
+            for dst, src in zip(gbufs, grads):
+                dst.copy_(src)
+            torch.cuda.synchronize()
         try:
             for r in range(N):
                 with torch.cuda.stream(streams[r]):
-                    dps[r].step(grads[r], lr=lr)
+                    dps[r].step(gbufs[r] if graphed else grads[r], lr=lr)
             torch.cuda.synchronize()
         except Exception as e:
             raise AssertionError(f"step {step}: {e}; watchdog report {B.peer_timeout_report()}") from e
@@ -288,3 +295,12 @@ def test_loopback_graph_replay_allreduce(B, N, oneshot, jit):
             mus[t] = OP.mu_update(mus[t], ref["sat"], ref["n"], False)
             assert F32(bufs[0]["mu"][t].item()) == mus[t], (step, t)
     assert B.peer_timeout_report()[0] == 0
+
+
+@pytest.mark.parametrize("variant", ["p2p", "p2p_oneshot", "zero"])
+def test_loopback_graphed_step(B, variant):
+    """fp8lm_dp_step_graphed across N = 2 ranks on one GPU: each rank's step captured on
+    its own stream (flag epochs from the pads' device counters, AdamW scalars patched per
+    replay), bit-exact against the oracle over 5 steps."""
+    mode = variant.split("_")[0]
+    run_loopback(B, RAGGED, mode, 2, steps=5, specials=_huge, oneshot="oneshot" in variant, graphed=True)

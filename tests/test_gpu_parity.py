@@ -89,7 +89,8 @@ RAGGED = [3, 16, 17, 64, 1000, 16384, 16385, 40000, 70001]
 
 
 def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float32,
-                     specials=None, amp=None, check_tensors=None, fused=True, delayed=False):
+                     specials=None, amp=None, check_tensors=None, fused=True, delayed=False,
+                     graphed=False):
     """Run the device path for `steps` steps and the oracle on the same inputs; compare
     every per-tensor output of every step.  check_tensors: oracle runs only on this
     subset (valid because nothing couples two tensors except the skip flag, and the
@@ -101,7 +102,8 @@ def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float3
         if v.numel():
             synth.fill_weights(v, t)
     dp = B.FP8DataParallel(plan, w0, lr=lr, fused=fused,
-                           state_scaling="delayed" if delayed else "jit")
+                           state_scaling="delayed" if delayed else "jit", graphed=graphed)
+    gbuf = None          # graphed: the captured step reads the same gradient buffers every step
     sub = list(range(plan.T)) if check_tensors is None else list(check_tensors)
     ref_states = R.oracle_init(plan, w0, sub)
     mus = [F32(1.0)] * len(sub)
@@ -112,7 +114,15 @@ def _run_and_compare(B, numels, mode, nranks, steps, lr=3e-4, dtype=torch.float3
     for step in range(1, steps + 1):
         grads = R.make_grads(plan, nranks, step, DEV, dtype,
                              specials=(lambda f, r: specials(f, r, step)) if specials else None, amp=amp)
-        dp.step(grads if mode == B.MODE_SIMULATED else grads[0], lr=lr)
+        if graphed:
+            if gbuf is None:
+                gbuf = [g.clone() for g in grads]
+            for dst, src in zip(gbuf, grads):
+                dst.copy_(src)
+            torch.cuda.synchronize()
+            dp.step(gbuf if mode == B.MODE_SIMULATED else gbuf[0], lr=lr)
+        else:
+            dp.step(grads if mode == B.MODE_SIMULATED else grads[0], lr=lr)
         torch.cuda.synchronize()
         per_rank = [[R.to_np_f32(g[plan.offsets[t]: plan.offsets[t] + plan.numels[t]]) for t in sub]
                     for g in grads]
@@ -370,3 +380,23 @@ def test_mu_reaches_cap_on_device(B):
             assert got[1] == F32(2.0), (step, got)
         if step == 7:
             assert got[1] == F32(1.0), got
+
+
+@pytest.mark.parametrize("case", ["local", "local_delayed", "local_bf16_skip", "simulated2"])
+def test_graphed_step(B, case):
+    """fp8lm_dp_step_graphed: eager on the first call, captured on the second, replayed from
+    the third with the step's scalars (bias correction, history slot) patched into the
+    AdamW nodes — bit-exact against the oracle every step (mu dynamics, a skip step, the
+    16-slot history wrapping with delayed scaling, the fused simulated reduce)."""
+    if case == "local":
+        _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=6, graphed=True)
+    elif case == "local_delayed":
+        _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=20, delayed=True, graphed=True)
+    elif case == "local_bf16_skip":
+        def specials(flat, r, step):
+            if step == 4:
+                flat[11] = float("inf")
+        _run_and_compare(B, RAGGED, B.MODE_LOCAL, 1, steps=6, dtype=torch.bfloat16, specials=specials,
+                         graphed=True)
+    else:
+        _run_and_compare(B, RAGGED, B.MODE_SIMULATED, 2, steps=5, graphed=True)
