@@ -194,3 +194,19 @@ def test_commstats_metrics_host(B):
     assert metrics(1.0, 0.0, 0, 0, 0)[0] == math.inf and metrics(1.0, 0.0, 0, 0, 0)[1:] == [0.0, 0.0]
     assert math.isnan(metrics(0.0, 0.0, 0, 0, 10)[0])
     assert metrics(0.0, 2.0, 0, 0, 10)[0] == -math.inf
+
+
+def test_bucket_split_contiguous_balanced(B):
+    """The split step's buckets (BucketedDP): contiguous groups covering every tensor once,
+    in order, with about equal parameter counts (GPT-7B set into 6 buckets)."""
+    import synth
+    numels = [s.numel for s in synth.gpt_gradient_set("gpt-7b")]
+    for nb in (1, 2, 3, 6, 8):
+        groups = B.bucket_split(numels, nb)
+        assert len(groups) == nb
+        flat = [t for g in groups for t in g]
+        assert flat == list(range(len(numels)))
+        loads = [sum(numels[t] for t in g) for g in groups]
+        # the largest tensor (the embedding, 3 % of the set) bounds the imbalance
+        assert max(loads) <= sum(numels) / nb + max(numels)
+    assert B.bucket_split([5, 1], 4) == [[0], [1]]
