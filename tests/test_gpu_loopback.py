@@ -48,7 +48,7 @@ def B():
 
 
 def run_loopback(B, numels, mode, N, steps, fused=True, delayed=False, lr=3e-4, sub=None,
-                 specials=None, oneshot=False, graphed=False):
+                 specials=None, oneshot=False, graphed=False, dtype=torch.float32):
     """oneshot: mode P2P's small-message exchange (fp8lm_plan_set_oneshot); off by
     default so that these small sets take the reduce-scatter / all-gather kernels."""
     import synth
@@ -77,7 +77,7 @@ def run_loopback(B, numels, mode, N, steps, fused=True, delayed=False, lr=3e-4, 
     hists = [OA.init_history(st) for st in ref_states] if delayed else None
     msgs = []
     for step in range(1, steps + 1):
-        grads = R.make_grads(plan, N, step, "cuda",
+        grads = R.make_grads(plan, N, step, "cuda", dtype,
                              specials=(lambda f, r: specials(f, r, step)) if specials else None)
         torch.cuda.synchronize()
         if graphed:      # the captured steps read the same buffers every step
@@ -304,3 +304,11 @@ def test_loopback_graphed_step(B, variant):
     replay), bit-exact against the oracle over 5 steps."""
     mode = variant.split("_")[0]
     run_loopback(B, RAGGED, mode, 2, steps=5, specials=_huge, oneshot="oneshot" in variant, graphed=True)
+
+
+@pytest.mark.parametrize("variant", ["p2p", "p2p_oneshot", "zero"])
+def test_loopback_bf16_gradients(B, variant):
+    """bf16 gradients (exact widening) through the multi-GPU kernels: the exchange's
+    quantize, the one-kernel small-message path (k_oneshot_full), ZeRO's owner reduce."""
+    run_loopback(B, RAGGED, variant.split("_")[0], 2, steps=3, specials=_huge, oneshot="oneshot" in variant,
+                 dtype=torch.bfloat16)
