@@ -59,6 +59,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     """Each source compiles to an object in parallel (kernels.cu dominates), then one link.
     out / defines: an experiment build (A/B runs load it through FP8LM_LIB)."""
     lib_out = out or LIB
+    if out: os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
     if not force and out is None and not defines and not needs_rebuild():
         return LIB
     inc, lib = nccl_dirs()
