@@ -7,6 +7,8 @@ For every FP8 payload size n (bytes = elements) it times, max over ranks, CUDA e
               from an fp32 gradient: up to 1 MiB ONE kernel (amax, MIN of the scales
               through the peer pads, the one-shot exchange), above it amax + quantize + the
               fused peer-memory reduce-scatter + rank-order reduce + all-gather
+  p2p_raw_full — up to 1 MiB: the one-handshake raw one-shot (k_oneshot_raw: every rank
+              pulls the fp32 gradients and encodes them itself)
   p2p_rsag_full — up to 1 MiB: the same with the one-shot path off (quantize + RS + AG)
   p2p_xchg  — the fused exchange kernel alone (k_reduce_p2p, library launch tracing)
   nccl_full — the same arithmetic with NCCL transport (mode NCCL)
@@ -69,13 +71,15 @@ def main():
         g = torch.empty(n, dtype=torch.float32, device="cuda")
         synth.fill_gradient(g, 1, 0, rank, amp=1e-3)
         res = {}
-        for mode_name, mode, oneshot in (("p2p", B.MODE_P2P, True), ("p2p_rsag", B.MODE_P2P, False),
-                                         ("nccl", B.MODE_NCCL, False)):
-            if mode_name == "p2p_rsag" and n > (1 << 20):
-                continue                       # above 1 MiB both p2p rows are the RS+AG path
+        for mode_name, mode, oneshot in (("p2p_raw", B.MODE_P2P, "raw"), ("p2p", B.MODE_P2P, True),
+                                         ("p2p_rsag", B.MODE_P2P, False), ("nccl", B.MODE_NCCL, False)):
+            if mode_name in ("p2p_rsag", "p2p_raw") and n > (1 << 20):
+                continue                       # above 1 MiB the p2p rows are the RS+AG path
             plan = B.Plan([n], mode=mode, nranks=N, rank=rank)
             if mode == B.MODE_P2P:
                 plan.set_oneshot((1 << 20) if oneshot else 0)
+                # p2p_raw: one handshake (k_oneshot_raw); p2p: two (k_oneshot_full)
+                plan.set_oneshot_raw((1 << 20) if oneshot == "raw" else 0)
                 plan.peer_setup(comm)
                 g8 = plan.peer_g8()
                 c = None

@@ -208,6 +208,18 @@ int fp8lm_peer_timeout_report(uint32_t* out4);
  * same value.  Host call; EINVAL on a NULL plan or a negative size. */
 int fp8lm_plan_set_oneshot(fp8lm_plan* plan, int64_t max_bytes);
 
+/* Mode P2P, the smallest messages: a one-shot plan whose code buffer is at most max_bytes
+ * (default 1 MiB / (4 (N-1)): 256 KiB at N = 2, 85 KiB at N = 4 — where it measured faster;
+ * 0 = never; effective only for plans of at most 1 MiB, whose send
+ * window fp8lm_peer_setup sizes for it) runs fp8lm_allreduce_jit / fp8lm_dp_step with the
+ * RAW one-shot kernel: each rank copies its gradient (fp32 / bf16 as given) into its send
+ * window during the amax pass, the Eq. 4 MIN handshake publishes the copy with the scale,
+ * and every rank pulls every rank's gradient and encodes it itself with s_g (Eq. 5 — the
+ * same codes) before the rank-order sum: one cross-rank handshake and no quantize pass,
+ * for (N-1) n sizeof(src) bytes of NVLink per rank.  Same results bit for bit.  Every rank
+ * must set the same value.  Host call; EINVAL on a NULL plan or a negative size. */
+int fp8lm_plan_set_oneshot_raw(fp8lm_plan* plan, int64_t max_bytes);
+
 /* Mode P2P: this rank's g8 window (device); pass it as g8 to the calls below.  NULL if
  * fp8lm_peer_setup has not run. */
 uint8_t* fp8lm_peer_g8(const fp8lm_plan* plan);
@@ -272,7 +284,8 @@ int fp8lm_grad_allreduce(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
 /* (2) + (3) in one call: fp8lm_amax_scale_sync then fp8lm_grad_allreduce, same
  * arguments and results.  Mode P2P with a small plan (fp8lm_plan_set_oneshot): ONE kernel
  * — amax, the Eq. 4 MIN through the pads, the one-shot exchange — one launch and two
- * cross-rank handshakes per step (config C5's small messages).  Other modes / sizes: the
+ * cross-rank handshakes per step (config C5's small messages); one handshake for the
+ * smallest plans (fp8lm_plan_set_oneshot_raw).  Other modes / sizes: the
  * two calls. */
 int fp8lm_allreduce_jit(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t src_dtype,
                         float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,

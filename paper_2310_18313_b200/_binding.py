@@ -77,6 +77,7 @@ _sig("fp8lm_peer_setup_loopback", C.c_int, C.POINTER(_p), _i32, _p)
 _sig("fp8lm_set_peer_timeout", C.c_int, _f64)
 _sig("fp8lm_peer_timeout_report", C.c_int, C.POINTER(C.c_uint32))
 _sig("fp8lm_plan_set_oneshot", C.c_int, _p, _i64)
+_sig("fp8lm_plan_set_oneshot_raw", C.c_int, _p, _i64)
 _sig("fp8lm_peer_g8", _p, _p)
 _sig("fp8lm_peer_w8", _p, _p)
 _sig("fp8lm_peer_w8_scalars", _p, _p)
@@ -284,6 +285,10 @@ class Plan:
     def set_oneshot(self, max_bytes: int):
         """Mode P2P: the one-shot small-message exchange up to max_bytes (0 = off)."""
         _check(lib.fp8lm_plan_set_oneshot(self.handle, int(max_bytes)), "fp8lm_plan_set_oneshot")
+
+    def set_oneshot_raw(self, max_bytes: int):
+        """Mode P2P: the one-handshake raw one-shot up to max_bytes (0 = off; plans <= 1 MiB)."""
+        _check(lib.fp8lm_plan_set_oneshot_raw(self.handle, int(max_bytes)), "fp8lm_plan_set_oneshot_raw")
 
     def _window(self, ptr, n, typestr):
         if not ptr:

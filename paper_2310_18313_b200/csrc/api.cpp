@@ -231,6 +231,7 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
   p->mode = mode;
   p->nranks = nranks;
   p->rank = dist ? rank : 0;
+  if (nranks > 1) p->oneshot_raw_max_bytes = FP8LM_ONESHOT_RAW_PULL / ((int64_t)(nranks - 1) * 4);
   p->numel.assign(numels, numels + T);
   p->offset.resize(T);
   p->item_start.resize(T + 1);
@@ -350,8 +351,13 @@ int32_t fp8lm_plan_owned_count(const fp8lm_plan* p) {
 // ---------------------------------------------------------------- mode P2P windows
 // this rank's symmetric windows (send, g8, w8, pad), zeroed where a peer may read first
 static int peer_alloc(fp8lm_plan* p) {
-  const size_t win = (size_t)p->g8_bytes;
+  size_t win = (size_t)p->g8_bytes;
   const bool zero = p->mode == FP8LM_MODE_ZERO;
+  if (!zero && p->T > 0 && p->g8_bytes <= kRawAllocMax) {   // the raw one-shot's two copies
+    p->raw_off = (int64_t)round_up((int64_t)win, 256);
+    p->raw_half = (int64_t)round_up(p->total * (int64_t)sizeof(float), 256);
+    win = (size_t)(p->raw_off + 2 * p->raw_half);
+  }
   p->pad_bytes = pad_bytes_for(p->nranks, p->T);
   CUDA_TRY(cudaMalloc(&p->win_send, win));
   CUDA_TRY(cudaMalloc(&p->win_g8, zero ? 256 : win));     // ZERO: the owner's g8 is compact
@@ -509,6 +515,11 @@ float* fp8lm_peer_w8_scalars(const fp8lm_plan* p) {
 int fp8lm_plan_set_oneshot(fp8lm_plan* p, int64_t max_bytes) {
   if (!p || max_bytes < 0) return fail(FP8LM_EINVAL, "plan_set_oneshot: bad arguments");
   p->oneshot_max_bytes = max_bytes;
+  return FP8LM_OK;
+}
+int fp8lm_plan_set_oneshot_raw(fp8lm_plan* p, int64_t max_bytes) {
+  if (!p || max_bytes < 0) return fail(FP8LM_EINVAL, "plan_set_oneshot_raw: bad arguments");
+  p->oneshot_raw_max_bytes = max_bytes;
   return FP8LM_OK;
 }
 
@@ -929,8 +940,12 @@ int fp8lm_allreduce_jit(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
       return fail(FP8LM_EINVAL, "allreduce_jit: NULL output");
     if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "allreduce_jit: mode P2P needs g8 == fp8lm_peer_g8(plan)");
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
-    CUDA_TRY(launch_oneshot_full(p->dev, p2p_args(p), srcs[0], src_dtype, mu, amax_out, s_g, skip, g8, tail,
-                                 S(stream)));
+    if (p->raw_half > 0 && p->g8_bytes <= p->oneshot_raw_max_bytes)   // one handshake
+      CUDA_TRY(launch_oneshot_raw(p->dev, p2p_args(p), srcs[0], src_dtype, mu, amax_out, s_g, skip, g8, tail,
+                                  p->raw_off, p->raw_half, S(stream)));
+    else
+      CUDA_TRY(launch_oneshot_full(p->dev, p2p_args(p), srcs[0], src_dtype, mu, amax_out, s_g, skip, g8, tail,
+                                   S(stream)));
     return FP8LM_OK;
   }
   if ((rc = fp8lm_amax_scale_sync(p, comm, grads, src_dtype, mu, amax_out, s_g, skip, stream))) return rc;
@@ -1036,6 +1051,10 @@ static int split_xcap(const fp8lm_plan* p) {
   if (p->loopback_ctas) return p->loopback_ctas;
   return FP8LM_SPLIT_XCAP ? FP8LM_SPLIT_XCAP : 3 * num_sms() / 2;
 }
+#ifndef FP8LM_ZERO_P2_XS
+#define FP8LM_ZERO_P2_XS 1
+#endif
+static constexpr bool kZeroPass2OnXs = FP8LM_ZERO_P2_XS != 0;
 struct CapScope {
   LaunchPolicy saved;
   explicit CapScope(int ctas) : saved(launch_policy()) {
@@ -1098,6 +1117,7 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
       return fail(FP8LM_EINVAL, "dp_step: NULL argument");
     if (p->own->T > 0 && (!g8 || !aligned(g8, 256))) return fail(FP8LM_EINVAL, "dp_step: g8 NULL or misaligned");
     const TailArgs tail{p->nranks, skip, sat, g_scale, g_scale_inv, mu};
+    cudaStream_t ps = S(stream);   // the stream pass 2 (+ w8 broadcast) runs on
     if (phase != 2) {
       const void* srcs[1];
       int nsrc = 0;
@@ -1119,26 +1139,39 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
         CUDA_TRY((cudaError_t)rc);
       }
       if (phase == 1) {
-        CUDA_TRY(cudaEventRecord(p->ev_x, p->xs));
-        return FP8LM_OK;
+        if (!kZeroPass2OnXs) {
+          CUDA_TRY(cudaEventRecord(p->ev_x, p->xs));
+          return FP8LM_OK;
+        }
+        ps = p->xs;
       }
     } else {
       CUDA_TRY(cudaStreamWaitEvent(S(stream), p->ev_x, 0));
+      if (kZeroPass2OnXs) return FP8LM_OK;
     }
     // pass 2 on the owned tensors also stores every w8 group into every rank's window
-    // (the broadcast overlaps the HBM-bound pass); its last CTA publishes the scalars
+    // (the broadcast overlaps the HBM-bound pass); its last CTA publishes the scalars.
+    // In a split step it follows the owner reduce on the exchange stream: both are
+    // NVLink-bound, and there they overlap the other buckets' amax / quantize passes
     Pass2Ext ext;
     ext.bcast = p2p_args(p);
     ext.own_gpos = p->dev.own_gpos;
     ext.own2full = p->dev.own2full;
     ext.T_full = p->T;
-    if (p->own->dev.n_items > 0) {
-      CUDA_TRY(launch_adam(p->own->dev, g8, p->dev.gsinv_own, *m1, *v, *master, *w8, *hp, skip,
-                           S(stream), /*pass1=*/false, &ext));
-    } else {   // a rank that owns nothing still meets the others at flag W8
-      CUDA_TRY(launch_w8_bcast(p->dev, p->own->dev, ext.bcast, static_cast<const uint8_t*>(w8->data),
-                               *w8, S(stream)));
+    {
+      LaunchPolicy keep = launch_policy();
+      if (ps != S(stream)) launch_policy().max_ctas = split_xcap(p);
+      if (p->own->dev.n_items > 0) {
+        rc = launch_adam(p->own->dev, g8, p->dev.gsinv_own, *m1, *v, *master, *w8, *hp, skip, ps,
+                         /*pass1=*/false, &ext);
+      } else {   // a rank that owns nothing still meets the others at flag W8
+        rc = launch_w8_bcast(p->dev, p->own->dev, ext.bcast, static_cast<const uint8_t*>(w8->data),
+                             *w8, ps);
+      }
+      launch_policy() = keep;
+      CUDA_TRY((cudaError_t)rc);
     }
+    if (ps != S(stream)) CUDA_TRY(cudaEventRecord(p->ev_x, p->xs));
     return FP8LM_OK;
   }
   if (p->mode == FP8LM_MODE_P2P) {

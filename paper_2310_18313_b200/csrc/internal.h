@@ -135,6 +135,15 @@ struct TailArgs {
 
 }  // namespace fp8lm
 
+// raw one-shot sizes: the window copy is allocated for plans up to kRawAllocMax code bytes
+// and used, by default, while a rank's raw pull ((N-1) * 4 * n bytes) is at most
+// FP8LM_ONESHOT_RAW_PULL — measured (profiles/r2/c5_raw): the raw kernel wins up to 256K
+// elements at N = 2 and 64K at N = 4 (fp8lm_plan_set_oneshot_raw changes it per plan)
+#ifndef FP8LM_ONESHOT_RAW_PULL
+#define FP8LM_ONESHOT_RAW_PULL (1 << 20)
+#endif
+constexpr int64_t kRawAllocMax = 1 << 20;
+
 struct fp8lm_plan {
   int32_t T = 0;
   int32_t mode = 0;
@@ -169,6 +178,10 @@ struct fp8lm_plan {
   // mode P2P: a plan whose reduced codes fit in this many bytes takes the one-shot
   // exchange (fp8lm_plan_set_oneshot; default 1 MiB)
   int64_t oneshot_max_bytes = 1 << 20;
+  // raw one-shot (launch_oneshot_raw): the send window carries two fp32 copies of the set
+  // behind the codes when g8_bytes <= kRawAllocMax; used up to oneshot_raw_max_bytes
+  int64_t raw_off = 0, raw_half = 0;
+  int64_t oneshot_raw_max_bytes = 0;   // set by fp8lm_plan_create from N
   // split step (fp8lm_dp_step_split): the exchange stream and its two events
   cudaStream_t xs = nullptr;
   cudaEvent_t ev_q = nullptr, ev_x = nullptr;
@@ -228,6 +241,11 @@ cudaError_t launch_oneshot(const DevPlan& p, const P2PArgs& x, const void* src, 
 cudaError_t launch_oneshot_full(const DevPlan& p, const P2PArgs& x, const void* src, int src_dtype,
                                 const float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
                                 const TailArgs& tail, cudaStream_t s);
+// the same with ONE cross-rank handshake: the gradient copied into the send window's raw
+// half (epoch & 1) at raw_off + half * raw_half; every rank pulls and encodes every rank's
+cudaError_t launch_oneshot_raw(const DevPlan& p, const P2PArgs& x, const void* src, int src_dtype,
+                               const float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
+                               const TailArgs& tail, int64_t raw_off, int64_t raw_half, cudaStream_t s);
 // mode ZERO: owner reduce over the compact sub-plan `o` (items), tails on the full plan `p`
 cudaError_t launch_reduce_owner(const DevPlan& p, const DevPlan& o, const P2PArgs& x, uint8_t* g8,
                                 const float* s_g, const TailArgs& tail, cudaStream_t s);

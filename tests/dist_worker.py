@@ -38,6 +38,7 @@ def main():
                     help="the three ABI calls instead of fp8lm_dp_step")
     ap.add_argument("--delayed", action="store_true", help="delayed state scaling (R25-R27)")
     ap.add_argument("--oneshot", action="store_true", help="mode P2P: the one-shot small-message exchange")
+    ap.add_argument("--raw", action="store_true", help="with --oneshot: the one-handshake raw one-shot")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -49,6 +50,7 @@ def main():
     mode = {"p2p": B.MODE_P2P, "nccl": B.MODE_NCCL, "zero": B.MODE_ZERO}[args.mode]
     plan = B.Plan(NUMELS, mode=mode, nranks=N, rank=rank)
     plan.set_oneshot(1 << 40 if args.oneshot else 0)
+    plan.set_oneshot_raw(1 << 40 if args.raw else 0)
     w0 = plan.flat(torch.float32)
     for t, v in enumerate(plan.views(w0)):
         synth.fill_weights(v, t)
@@ -89,7 +91,7 @@ def main():
         print(m, flush=True)
     if rank == 0:
         tag = args.mode.upper() + ("_UNFUSED" if args.unfused else "") + ("_DELAYED" if args.delayed else "") + \
-            ("_ONESHOT" if args.oneshot else "")
+            ("_ONESHOT" if args.oneshot else "") + ("_RAW" if args.raw else "")
         print(f"{tag} parity N={N}: {'OK' if flag.item() == 1 else 'MISMATCH'}", flush=True)
     comm.close()
     dist.destroy_process_group()

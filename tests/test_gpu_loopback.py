@@ -50,12 +50,15 @@ def B():
 def run_loopback(B, numels, mode, N, steps, fused=True, delayed=False, lr=3e-4, sub=None,
                  specials=None, oneshot=False, graphed=False, dtype=torch.float32):
     """oneshot: mode P2P's small-message exchange (fp8lm_plan_set_oneshot); off by
-    default so that these small sets take the reduce-scatter / all-gather kernels."""
+    default so that these small sets take the reduce-scatter / all-gather kernels.
+    True: the two-handshake one-shot (raw variant off); "raw": the one-handshake raw
+    one-shot (fp8lm_plan_set_oneshot_raw) where the call is fp8lm_allreduce_jit / dp_step."""
     import synth
     bmode = {"p2p": B.MODE_P2P, "zero": B.MODE_ZERO}[mode]
     plans = [B.Plan(numels, mode=bmode, nranks=N, rank=r) for r in range(N)]
     for p_ in plans:
         p_.set_oneshot(1 << 40 if oneshot else 0)
+        p_.set_oneshot_raw(1 << 40 if oneshot == "raw" else 0)
     B.peer_setup_loopback(plans)
     streams = [torch.cuda.Stream() for _ in range(N)]
     w0 = plans[0].flat(torch.float32)
@@ -124,13 +127,16 @@ def test_loopback_bit_exact(B, N, variant):
 
 
 @pytest.mark.parametrize("N", [2, 3, 4])
-@pytest.mark.parametrize("variant", ["fused", "unfused", "delayed"])
+@pytest.mark.parametrize("variant", ["fused", "unfused", "delayed", "raw", "raw_delayed"])
 def test_loopback_oneshot(B, N, variant):
     """Mode P2P's one-shot small-message exchange (k_oneshot: quantize, one handshake,
     every rank pulls and reduces the whole set): bit-exact through fp8lm_dp_step (then
-    both AdamW passes locally), the three calls and delayed scaling."""
-    run_loopback(B, RAGGED, "p2p", N, steps=3, fused=variant != "unfused", delayed=variant == "delayed",
-                 specials=_huge, oneshot=True)
+    both AdamW passes locally), the three calls and delayed scaling.  raw: the
+    one-handshake kernel k_oneshot_raw (every rank pulls the gradients and encodes them
+    itself; the window copy alternates halves step by step, so 4 steps wrap it twice)."""
+    raw = variant.startswith("raw")
+    run_loopback(B, RAGGED, "p2p", N, steps=4 if raw else 3, fused=variant != "unfused",
+                 delayed=variant.endswith("delayed"), specials=_huge, oneshot="raw" if raw else True)
 
 
 @pytest.mark.parametrize("mode", ["p2p", "zero"])
@@ -232,8 +238,8 @@ def test_loopback_split_buckets(B, N, variant):
 
 
 @pytest.mark.parametrize("N", [2, 4])
-@pytest.mark.parametrize("oneshot,jit", [(True, False), (False, False), (True, True), (False, True)],
-                         ids=["oneshot", "rsag", "oneshot_jit", "rsag_jit"])
+@pytest.mark.parametrize("oneshot,jit", [(True, False), (False, False), (True, True), (False, True), ("raw", True)],
+                         ids=["oneshot", "rsag", "oneshot_jit", "rsag_jit", "oneshot_raw_jit"])
 def test_loopback_graph_replay_allreduce(B, N, oneshot, jit):
     """The P2P exchange captured in a CUDA graph (one per rank, on its stream) and
     replayed: fp8lm_amax_scale_sync + fp8lm_grad_allreduce read their flag epochs from the
@@ -244,6 +250,7 @@ def test_loopback_graph_replay_allreduce(B, N, oneshot, jit):
     plans = [B.Plan(RAGGED, mode=B.MODE_P2P, nranks=N, rank=r) for r in range(N)]
     for p_ in plans:
         p_.set_oneshot(1 << 40 if oneshot else 0)
+        p_.set_oneshot_raw(1 << 40 if oneshot == "raw" else 0)
     B.peer_setup_loopback(plans)
     plan = plans[0]
     T = plan.T
@@ -273,7 +280,7 @@ def test_loopback_graph_replay_allreduce(B, N, oneshot, jit):
             call(r)
     torch.cuda.synchronize()
     mus = [F32(1.0)] * T
-    for step in range(1, 4):
+    for step in range(1, 5):
         grads = R.make_grads(plan, N, step, "cuda", specials=lambda f, r: _huge(f, r, step))
         for r in range(N):
             bufs[r]["g"].copy_(grads[r])
@@ -297,18 +304,22 @@ def test_loopback_graph_replay_allreduce(B, N, oneshot, jit):
     assert B.peer_timeout_report()[0] == 0
 
 
-@pytest.mark.parametrize("variant", ["p2p", "p2p_oneshot", "zero"])
+@pytest.mark.parametrize("variant", ["p2p", "p2p_oneshot", "p2p_oneshotraw", "zero"])
 def test_loopback_graphed_step(B, variant):
     """fp8lm_dp_step_graphed across N = 2 ranks on one GPU: each rank's step captured on
     its own stream (flag epochs from the pads' device counters, AdamW scalars patched per
     replay), bit-exact against the oracle over 5 steps."""
     mode = variant.split("_")[0]
-    run_loopback(B, RAGGED, mode, 2, steps=5, specials=_huge, oneshot="oneshot" in variant, graphed=True)
+    run_loopback(B, RAGGED, mode, 2, steps=5, specials=_huge, oneshot=_oneshot_arg(variant), graphed=True)
 
 
-@pytest.mark.parametrize("variant", ["p2p", "p2p_oneshot", "zero"])
+def _oneshot_arg(variant):
+    return "raw" if "oneshotraw" in variant else "oneshot" in variant
+
+
+@pytest.mark.parametrize("variant", ["p2p", "p2p_oneshot", "p2p_oneshotraw", "zero"])
 def test_loopback_bf16_gradients(B, variant):
     """bf16 gradients (exact widening) through the multi-GPU kernels: the exchange's
     quantize, the one-kernel small-message path (k_oneshot_full), ZeRO's owner reduce."""
-    run_loopback(B, RAGGED, variant.split("_")[0], 2, steps=3, specials=_huge, oneshot="oneshot" in variant,
+    run_loopback(B, RAGGED, variant.split("_")[0], 2, steps=3, specials=_huge, oneshot=_oneshot_arg(variant),
                  dtype=torch.bfloat16)

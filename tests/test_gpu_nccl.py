@@ -41,7 +41,7 @@ def _port():
 
 
 @pytest.mark.parametrize("mode", ["nccl", "p2p", "p2p_unfused", "zero", "zero_unfused", "p2p_delayed",
-                                  "zero_delayed", "p2p_oneshot", "p2p_unfused_oneshot"])
+                                  "zero_delayed", "p2p_oneshot", "p2p_unfused_oneshot", "p2p_oneshot_raw"])
 @pytest.mark.parametrize("n", [2, 4])
 def test_multi_gpu_bit_exact(n, mode):
     if _ngpus() < n:
@@ -50,7 +50,8 @@ def test_multi_gpu_bit_exact(n, mode):
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "dist_worker.py"), "--steps", "3",
            "--mode", mode.split("_")[0]] + (["--unfused"] if "unfused" in mode else []) + \
-          (["--delayed"] if "delayed" in mode else []) + (["--oneshot"] if "oneshot" in mode else [])
+          (["--delayed"] if "delayed" in mode else []) + (["--oneshot"] if "oneshot" in mode else []) + \
+          (["--raw"] if "raw" in mode else [])
     env = dict(os.environ)
     for _ in range(3):          # a freshly probed port can be taken before torchrun binds it
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
