@@ -357,8 +357,9 @@ int fp8lm_dp_step(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t
  * is a plan over a subset of the tensors (its own windows, flags and epochs).  phase 1:
  * amax + scale MIN + quantize on `stream`, then the exchange kernel (reduce-scatter +
  * rank-order reduce + Adam pass 1 on the own shard; ZERO: the owner reduce + pass 1) on
- * the plan's own high-priority exchange stream; phase 2: `stream` waits for that
- * exchange, then the AdamW pass with the pulled all-gather (ZERO: + w8 broadcast).  A
+ * the plan's own high-priority exchange stream (ZERO: followed there by the owner's pass 2
+ * + w8 broadcast, NVLink-bound like the owner reduce); phase 2: `stream` waits for that
+ * exchange, then (P2P) the AdamW pass with the pulled all-gather.  A
  * caller with buckets b = 0..B-1 issues phase 1 for every bucket, then phase 2 for every
  * bucket: the exchange of bucket b overlaps the amax / quantize of b+1 and pass 2 of b-1.
  * Same arguments and results as fp8lm_dp_step (comm unused: modes P2P / ZERO only; ZERO
