@@ -272,9 +272,10 @@ int fp8lm_amax_scale_sync(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
  * Mode P2P: g8 must be fp8lm_peer_g8(plan); one kernel reads every rank's quantized
  * shard over NVLink, reduces in rank order and stores the result into every rank's g8
  * (reduce-scatter + all-gather fused), with sys-scope flag barriers in the peers' pads.
- * Mode ZERO: g8 is this rank's COMPACT buffer (fp8lm_plan_owned_total bytes); the kernel
- * reduces, for each owned tensor, every rank's codes straight from their send windows
- * (no all-gather: only the owner needs them).  sat / mu / g_scale / g_scale_inv stay
+ * Mode ZERO: g8 is this rank's COMPACT buffer (fp8lm_plan_owned_total bytes); every
+ * rank's quantize pushes each code into its owner's window (slot = the rank, in the
+ * owner's compact layout) and the owner reduces its whole tensors from those N local
+ * slots (no all-gather: only the owner needs them).  sat / mu / g_scale / g_scale_inv stay
  * full [T] arrays, replicated on every rank. */
 int fp8lm_grad_allreduce(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads,
                          int32_t src_dtype, const float* s_g, const int32_t* skip,
@@ -358,7 +359,7 @@ int fp8lm_dp_step(fp8lm_plan* plan, fp8lm_comm* comm, const void* grads, int32_t
  * amax + scale MIN + quantize on `stream`, then the exchange kernel (reduce-scatter +
  * rank-order reduce + Adam pass 1 on the own shard; ZERO: the owner reduce + pass 1) on
  * the plan's own high-priority exchange stream (ZERO: followed there by the owner's pass 2
- * + w8 broadcast, NVLink-bound like the owner reduce); phase 2: `stream` waits for that
+ * + w8 broadcast, NVLink-bound); phase 2: `stream` waits for that
  * exchange, then (P2P) the AdamW pass with the pulled all-gather.  A
  * caller with buckets b = 0..B-1 issues phase 1 for every bucket, then phase 2 for every
  * bucket: the exchange of bucket b overlaps the amax / quantize of b+1 and pass 2 of b-1.

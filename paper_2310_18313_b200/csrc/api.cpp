@@ -301,6 +301,19 @@ int fp8lm_plan_create(int32_t T, const int64_t* numels, int32_t mode, int32_t nr
     if (rc) { delete p; return rc; }
     p->full2own_off.assign(std::max(T, 1), -1);
     for (size_t j = 0; j < p->own2full.size(); ++j) p->full2own_off[p->own2full[j]] = p->own->offset[j];
+    // A3's push layout: every rank quantizes tensor t straight into slot `rank` of its
+    // owner's window, in the owner's compact layout (the same Alg. 1 packing every rank
+    // computes), so the owner reduce reads N local slots instead of pulling over NVLink
+    std::vector<int64_t> qtot(nranks, 0), coff(std::max(T, 1), 0);
+    for (int t = 0; t < T; ++t) {
+      coff[t] = qtot[p->owner[t]];
+      qtot[p->owner[t]] += round_up(p->numel[t], FP8LM_ALIGN_ELEMS);
+    }
+    if (qtot[p->rank] != p->own->total) { delete p; return fail(FP8LM_EINVAL, "plan_create: owned layout mismatch"); }
+    p->push_base.assign(std::max(T, 1), 0);
+    for (int t = 0; t < T; ++t) p->push_base[t] = (int64_t)p->rank * qtot[p->owner[t]] + coff[t] - p->offset[t];
+    p->off_push_base = take(sizeof(int64_t) * std::max(T, 1));
+    p->off_owner_of = take(sizeof(int32_t) * std::max(T, 1));
     const size_t To = std::max<size_t>(p->own2full.size(), 1);
     p->off_own_ws = take(p->own->ws_bytes);
     p->off_own_gpos = take(sizeof(int64_t) * To);
@@ -351,8 +364,9 @@ int32_t fp8lm_plan_owned_count(const fp8lm_plan* p) {
 // ---------------------------------------------------------------- mode P2P windows
 // this rank's symmetric windows (send, g8, w8, pad), zeroed where a peer may read first
 static int peer_alloc(fp8lm_plan* p) {
-  size_t win = (size_t)p->g8_bytes;
   const bool zero = p->mode == FP8LM_MODE_ZERO;
+  // ZERO: N slots of this rank's compact (owned) layout, written by every rank's quantize
+  size_t win = zero ? std::max<size_t>((size_t)p->nranks * p->own->total, 256) : (size_t)p->g8_bytes;
   if (!zero && p->T > 0 && p->g8_bytes <= kRawAllocMax) {   // the raw one-shot's two copies
     p->raw_off = (int64_t)round_up((int64_t)win, 256);
     p->raw_half = (int64_t)round_up(p->total * (int64_t)sizeof(float), 256);
@@ -583,7 +597,16 @@ int fp8lm_plan_bind(fp8lm_plan* p, void* ws, size_t ws_bytes, void* stream) {
       CUDA_TRY(cudaMemcpyAsync(b + p->off_own_gpos, p->own_gpos.data(), sizeof(int64_t) * To, cudaMemcpyHostToDevice, s));
       CUDA_TRY(cudaMemcpyAsync(b + p->off_own2full, p->own2full.data(), sizeof(int32_t) * To, cudaMemcpyHostToDevice, s));
     }
+    if (p->T > 0) {
+      CUDA_TRY(cudaMemcpyAsync(b + p->off_push_base, p->push_base.data(), sizeof(int64_t) * p->T,
+                               cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(b + p->off_owner_of, p->owner.data(), sizeof(int32_t) * p->T,
+                               cudaMemcpyHostToDevice, s));
+    }
     CUDA_TRY(cudaStreamSynchronize(s));
+    d.push_base = reinterpret_cast<const int64_t*>(b + p->off_push_base);
+    d.owner_of = reinterpret_cast<const int32_t*>(b + p->off_owner_of);
+    d.own_slot = p->own->total;
     d.T_own = (int32_t)To;
     d.own_gpos = reinterpret_cast<const int64_t*>(b + p->off_own_gpos);
     d.own2full = reinterpret_cast<const int32_t*>(b + p->off_own2full);
@@ -877,9 +900,9 @@ int fp8lm_grad_allreduce(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int
     uint8_t* dst[1] = {g8};
     CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, &tail, s));
   } else if (p->mode == FP8LM_MODE_ZERO) {
-    uint8_t* dst[1] = {p->win_send};
-    CUDA_TRY(launch_quantize(d, srcs, dst, 1, src_dtype, s_g, nullptr, s));
-    // each owner reduces its whole tensors from every rank's send window
+    if (!p->p2p_ready) return fail(FP8LM_EINVAL, "grad_allreduce: mode ZERO needs fp8lm_peer_setup first");
+    CUDA_TRY(launch_quantize_push(d, p2p_args(p), srcs[0], src_dtype, s_g, s));
+    // each owner reduces its whole tensors from the N slots of its window
     CUDA_TRY(launch_reduce_owner(d, p->own->dev, p2p_args(p), g8, s_g, tail, s));
   } else if (p->mode == FP8LM_MODE_P2P) {
     if (g8 != p->win_g8) return fail(FP8LM_EINVAL, "grad_allreduce: mode P2P needs g8 == fp8lm_peer_g8(plan)");
@@ -1122,8 +1145,7 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
       const void* srcs[1];
       int nsrc = 0;
       if ((rc = grad_sources(p, grads, src_dtype, srcs, &nsrc, "dp_step"))) return rc;
-      uint8_t* dst[1] = {p->win_send};
-      CUDA_TRY(launch_quantize(p->dev, srcs, dst, 1, src_dtype, s_g, nullptr, S(stream)));
+      CUDA_TRY(launch_quantize_push(p->dev, p2p_args(p), srcs[0], src_dtype, s_g, S(stream)));
       cudaStream_t xs = S(stream);
       if (phase == 1) {
         CUDA_TRY(cudaEventRecord(p->ev_q, S(stream)));

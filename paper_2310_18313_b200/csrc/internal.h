@@ -44,6 +44,12 @@ struct DevPlan {
   const int64_t* own_gpos;  // [T_own] full-layout offset of owned tensor j
   const int32_t* own2full;  // [T_own] its global index t
   float* gsinv_own;         // [T_own] compact copy of g_scale_inv (written by the reduce tail)
+  // mode ZERO push layout: rank r's codes of tensor t go to window(owner_of[t]) +
+  // push_base[t] + pos (slot r of the owner's compact layout); own_slot = this rank's
+  // slot size (its compact total), so slot r of its own window starts at r * own_slot
+  const int64_t* push_base; // [T]
+  const int32_t* owner_of;  // [T]
+  int64_t own_slot;
 };
 
 constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2, kCtrFix = 3, kCtrFixGen = 4, kCtrOneshot = 5,
@@ -204,6 +210,8 @@ struct fp8lm_plan {
   std::vector<int64_t> own_gpos, full2own_off;
   fp8lm_plan* own = nullptr;
   size_t off_own_ws = 0, off_own_gpos = 0, off_own2full = 0, off_gsinv_own = 0;
+  std::vector<int64_t> push_base;
+  size_t off_push_base = 0, off_owner_of = 0;
 };
 
 namespace fp8lm {
@@ -246,6 +254,10 @@ cudaError_t launch_oneshot_full(const DevPlan& p, const P2PArgs& x, const void* 
 cudaError_t launch_oneshot_raw(const DevPlan& p, const P2PArgs& x, const void* src, int src_dtype,
                                const float* mu, float* amax_out, float* s_g, int32_t* skip, uint8_t* g8,
                                const TailArgs& tail, int64_t raw_off, int64_t raw_half, cudaStream_t s);
+// mode ZERO: A3 pushing every code into its owner's window (slot = this rank), then one
+// system-scope fence per CTA so the owners' reduce (after its "ready" flag) sees them
+cudaError_t launch_quantize_push(const DevPlan& p, const P2PArgs& x, const void* src, int src_dtype,
+                                 const float* s_g, cudaStream_t s);
 // mode ZERO: owner reduce over the compact sub-plan `o` (items), tails on the full plan `p`
 cudaError_t launch_reduce_owner(const DevPlan& p, const DevPlan& o, const P2PArgs& x, uint8_t* g8,
                                 const float* s_g, const TailArgs& tail, cudaStream_t s);
