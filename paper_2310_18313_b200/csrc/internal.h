@@ -50,6 +50,8 @@ struct DevPlan {
   const int64_t* push_base; // [T]
   const int32_t* owner_of;  // [T]
   int64_t own_slot;
+  // mode P2P push layout: rank r's codes of shard q go to window(q) + r * shard + (pos - q * shard)
+  int64_t shard;
 };
 
 constexpr int kCtrAmax = 0, kCtrTail = 1, kCtrAdam = 2, kCtrFix = 3, kCtrFixGen = 4, kCtrOneshot = 5,
@@ -84,6 +86,10 @@ struct P2PArgs {
   uint32_t* pad;          // this rank's pad
   int rank;
   int nranks;
+  // mode P2P: 1 — this step's quantize pushed the codes into the shard owners' window
+  // slots (the reduce-scatter reads N local slots); 0 — each rank's codes are in its own
+  // send window, full layout (the reduce-scatter pulls them)
+  int slots = 0;
 };
 // the step's epoch (flags hold the epoch of their last signal) / the w8 epoch, from the
 // own pad's counters
@@ -256,8 +262,9 @@ cudaError_t launch_oneshot_raw(const DevPlan& p, const P2PArgs& x, const void* s
                                const TailArgs& tail, int64_t raw_off, int64_t raw_half, cudaStream_t s);
 // mode ZERO: A3 pushing every code into its owner's window (slot = this rank), then one
 // system-scope fence per CTA so the owners' reduce (after its "ready" flag) sees them
+// mode P2P (shard_slots): the same into slot `rank` of each shard owner's window
 cudaError_t launch_quantize_push(const DevPlan& p, const P2PArgs& x, const void* src, int src_dtype,
-                                 const float* s_g, cudaStream_t s);
+                                 const float* s_g, cudaStream_t s, bool shard_slots = false);
 // mode ZERO: owner reduce over the compact sub-plan `o` (items), tails on the full plan `p`
 cudaError_t launch_reduce_owner(const DevPlan& p, const DevPlan& o, const P2PArgs& x, uint8_t* g8,
                                 const float* s_g, const TailArgs& tail, cudaStream_t s);
