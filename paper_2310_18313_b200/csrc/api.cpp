@@ -1066,16 +1066,20 @@ static int split_resources(fp8lm_plan* p) {
 // beside the HBM passes of the other buckets instead of taking every slot (highest
 // stream priority) and serialising them; FP8LM_SPLIT_HCAP (CTAs per SM, 0 = off) caps the
 // HBM passes as well.  Measured at GPT-7B N = 4 with 4 buckets (profiles/r2/split):
-// 1 CTA/SM 29.5 ms, 1.25 30.0, 1.5 28.8, 2 28.5-30.0, uncapped 33.8, unsplit 31.5.
+// 1 CTA/SM 29.5 ms, 1.25 30.0, 1.5 28.8, 2 28.5-30.0, uncapped 33.8, unsplit 31.5.  At
+// N = 2 the exchange kernel also runs pass 1 on half the tensors (a quarter at N = 4) and
+// needs more room: 6 buckets, 1.25 CTAs/SM 30.9 ms, 1.5 30.3-30.6, 2 29.1-29.2
+// (profiles/r2/n2ab).
 #ifndef FP8LM_SPLIT_XCAP
-#define FP8LM_SPLIT_XCAP 0           /* 0: 3 * #SMs / 2 */
+#define FP8LM_SPLIT_XCAP 0           /* 0: 2 * #SMs at N = 2, 3 * #SMs / 2 above */
 #endif
 #ifndef FP8LM_SPLIT_HCAP
 #define FP8LM_SPLIT_HCAP 0
 #endif
 static int split_xcap(const fp8lm_plan* p) {
   if (p->loopback_ctas) return p->loopback_ctas;
-  return FP8LM_SPLIT_XCAP ? FP8LM_SPLIT_XCAP : 3 * num_sms() / 2;
+  if (FP8LM_SPLIT_XCAP) return FP8LM_SPLIT_XCAP;
+  return p->nranks <= 2 ? 2 * num_sms() : 3 * num_sms() / 2;
 }
 #ifndef FP8LM_ZERO_P2_XS
 #define FP8LM_ZERO_P2_XS 1
