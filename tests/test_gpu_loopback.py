@@ -126,6 +126,17 @@ def test_loopback_bit_exact(B, N, variant):
                  delayed="delayed" in variant, specials=_huge)
 
 
+@pytest.mark.parametrize("N", [3, 4])
+@pytest.mark.parametrize("variant", ["p2p", "p2p_unfused", "p2p_delayed", "zero", "zero_unfused"])
+def test_loopback_tiny_shards(B, N, variant):
+    """Shards smaller than a 16K-element work item: one item of the first tensor spans
+    several shards, so the pushing quantize (P2P whole step / three calls) sends its
+    16-code groups to several shard owners, and ZeRO owners get uneven loads."""
+    mode = variant.split("_")[0]
+    run_loopback(B, [20000, 5, 3000, 17, 64], mode, N, steps=3, fused="unfused" not in variant,
+                 delayed="delayed" in variant, specials=_huge)
+
+
 @pytest.mark.parametrize("N", [2, 3, 4])
 @pytest.mark.parametrize("variant", ["fused", "unfused", "delayed", "raw", "raw_delayed"])
 def test_loopback_oneshot(B, N, variant):
