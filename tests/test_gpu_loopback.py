@@ -126,6 +126,16 @@ def test_loopback_bit_exact(B, N, variant):
                  delayed="delayed" in variant, specials=_huge)
 
 
+@pytest.mark.parametrize("variant", ["p2p", "p2p_unfused", "p2p_delayed", "zero", "zero_unfused",
+                                     "p2p_oneshot", "p2p_oneshotraw"])
+def test_loopback_eight_ranks(B, variant):
+    """N = 8 (the largest group the kernels are instantiated for; gpurun offers at most 4
+    GPUs): the NR = 8 exchange, one-shot and owner kernels, bit-exact on every rank."""
+    mode = variant.split("_")[0]
+    run_loopback(B, RAGGED, mode, 8, steps=3, fused="unfused" not in variant, delayed="delayed" in variant,
+                 specials=_huge, oneshot=_oneshot_arg(variant))
+
+
 @pytest.mark.parametrize("N", [3, 4])
 @pytest.mark.parametrize("variant", ["p2p", "p2p_unfused", "p2p_delayed", "zero", "zero_unfused"])
 def test_loopback_tiny_shards(B, N, variant):
