@@ -54,6 +54,9 @@ def main():
     ap.add_argument("--max-log2", type=int, default=30)
     ap.add_argument("--stride", type=int, default=2)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--src-dtype", default="f32", choices=["f32", "bf16"],
+                    help="gradient dtype of the FP8 rows (A1-A5 from fp32 or from bf16); the "
+                         "NCCL rows are unchanged")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -70,6 +73,8 @@ def main():
         iters = max(5, min(args.iters, int(2e9 // n)))
         g = torch.empty(n, dtype=torch.float32, device="cuda")
         synth.fill_gradient(g, 1, 0, rank, amp=1e-3)
+        if args.src_dtype == "bf16":
+            g = g.to(torch.bfloat16)
         res = {}
         for mode_name, mode, oneshot in (("p2p_raw", B.MODE_P2P, "raw"), ("p2p", B.MODE_P2P, True),
                                          ("p2p_rsag", B.MODE_P2P, False), ("nccl", B.MODE_NCCL, False)):
@@ -132,6 +137,8 @@ def main():
             payload = n * (2 if impl.startswith("nccl_bf16") else 4 if impl == "nccl_f32" else 1)
             algbw = payload / (us * 1e-6) / 1e9
             row = {"config": "C5", "n_gpus": N, "elements": n, "fp8_bytes": n, "impl": impl,
+                   "src_dtype": {"nccl_bf16": "bf16", "nccl_bf16_graph": "bf16", "nccl_f32": "f32"}.get(impl, args.src_dtype),
+                   "nccl_algo": os.environ.get("NCCL_ALGO", "default"),
                    "us": us, "algbw_GBs": algbw, "busbw_GBs": algbw * busf,
                    "busbw_frac_of_900": algbw * busf / 900.0}
             rows.append(row)

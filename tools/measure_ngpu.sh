@@ -16,9 +16,13 @@ run 4 bench_7b_n4_unsplit bench.py --gpus 4 --steps 20 --warmup 5 --buckets 1 --
 run 4 bench_7b_n4_delayed bench.py --gpus 4 --steps 20 --warmup 5 --state-scaling delayed --no-e2e
 run 4 bench_7b_n4_nccl bench.py --gpus 4 --steps 10 --warmup 3 --exchange nccl --no-e2e
 run 4 bench_13b_n4_zero bench.py --gpus 4 --config gpt-13b --exchange zero --steps 10 --warmup 3 --buckets 4 --no-e2e
+run 4 bench_13b_n4_zero_unsplit bench.py --gpus 4 --config gpt-13b --exchange zero --steps 10 --warmup 3 --buckets 1 --no-e2e
 run 2 bench_125m_n2 bench.py --gpus 2 --config gpt-125m --no-e2e
 run 4 bench_125m_n4 bench.py --gpus 4 --config gpt-125m --no-e2e
 run 2 c5_n2 bench_c5.py --min-log2 10 --max-log2 30 --stride 2
 run 4 c5_n4 bench_c5.py --min-log2 10 --max-log2 30 --stride 2
+run 2 c5_n2_bf16src bench_c5.py --min-log2 10 --max-log2 30 --stride 4 --src-dtype bf16
+NCCL_ALGO=Ring run 4 c5_n4_ring bench_c5.py --min-log2 10 --max-log2 30 --stride 4
+NCCL_ALGO=NVLS run 4 c5_n4_nvls bench_c5.py --min-log2 10 --max-log2 30 --stride 4
 run 2 sp_n2 bench_sp.py
 run 4 sp_n4 bench_sp.py
