@@ -1081,10 +1081,6 @@ static int split_xcap(const fp8lm_plan* p) {
   if (FP8LM_SPLIT_XCAP) return FP8LM_SPLIT_XCAP;
   return p->nranks <= 2 ? 2 * num_sms() : 3 * num_sms() / 2;
 }
-#ifndef FP8LM_ZERO_P2_XS
-#define FP8LM_ZERO_P2_XS 1
-#endif
-static constexpr bool kZeroPass2OnXs = FP8LM_ZERO_P2_XS != 0;
 struct CapScope {
   LaunchPolicy saved;
   explicit CapScope(int ctas) : saved(launch_policy()) {
@@ -1167,16 +1163,12 @@ static int dp_step_impl(fp8lm_plan* p, fp8lm_comm* comm, const void* grads, int3
         launch_policy() = keep;
         CUDA_TRY((cudaError_t)rc);
       }
-      if (phase == 1) {
-        if (!kZeroPass2OnXs) {
-          CUDA_TRY(cudaEventRecord(p->ev_x, p->xs));
-          return FP8LM_OK;
-        }
-        ps = p->xs;
-      }
+      // split step: pass 2 follows on the exchange stream (GPT-13B N = 4, 4 buckets:
+      // 44.8 ms with it on the rank stream, 41.1-41.7 here; profiles/r2/zero_push)
+      if (phase == 1) ps = p->xs;
     } else {
       CUDA_TRY(cudaStreamWaitEvent(S(stream), p->ev_x, 0));
-      if (kZeroPass2OnXs) return FP8LM_OK;
+      return FP8LM_OK;
     }
     // pass 2 on the owned tensors also stores every w8 group into every rank's window
     // (the broadcast overlaps the HBM-bound pass); its last CTA publishes the scalars.
