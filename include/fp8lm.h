@@ -333,7 +333,9 @@ int fp8lm_adam_step_delayed(fp8lm_plan* plan, const uint8_t* g8, const float* g_
  * results are bit-identical to calling fp8lm_amax_scale_sync, fp8lm_grad_allreduce and
  * fp8lm_adam_step in sequence (same arguments).  Mode LOCAL: the codes of A3 are final
  * (N = 1), so the quantize kernel also runs Adam pass 1 on them (4 launches per step,
- * 26 B/param instead of 27).  Mode P2P: the exchange kernel runs Adam pass 1 on the
+ * 26 B/param instead of 27).  Mode P2P: the quantize pushes every 16-code group into
+ * slot `rank` of its shard owner's send window (the reduce-scatter's NVLink transfer
+ * rides on the quantize pass); the exchange kernel runs Adam pass 1 on the
  * elements of its own shard (1/N of pass 1 per rank) and combines the ranks' partial
  * state maxima through the pads; the all-gather (A5) is a PULL inside pass 2 (delayed
  * state scaling: inside the single pass), which reads each code from its owner's g8
