@@ -43,7 +43,7 @@ def timed(fn, iters, warm=3):
         fn()
     b.record()
     torch.cuda.synchronize()
-    t = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float64, device="cuda")
+    t = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float32, device="cuda")   # NVLS: no f64
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.item() * 1e3          # us
 
@@ -118,7 +118,7 @@ def main():
             prof = B.prof_read()
             if mode_name == "p2p" and "reduce_p2p" in prof:
                 t = torch.tensor([prof["reduce_p2p"]["ms"] / prof["reduce_p2p"]["launches"]],
-                                 dtype=torch.float64, device="cuda")
+                                 dtype=torch.float32, device="cuda")
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 res["p2p_xchg"] = t.item() * 1e3
             del plan, g8
