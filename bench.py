@@ -612,7 +612,9 @@ def main():
             roof["traffic"] = ent["dram_bytes_per_launch"]
             roof["traffic_source"] = f"profiles/{rnd}/ncu_traffic.json [{key}] ({ent['source']})"
             break
-    launches = int(sum(v["launches"] for v in ours.values()) / args.steps)
+    # our kernels launched inside the timed region (this rank): the instrumented pass runs
+    # the same K steps, so its count is the timed region's
+    launches = int(sum(v["launches"] for v in ours.values()))
     breakdown = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
                  for k, v in prof.items()}
     if world > 1:
@@ -686,6 +688,7 @@ def main():
                        "grad_sets_rotated": R, "grad_sets_antithetic": R % 2 == 0,
                        "hbm_frac_of_8tbs": value / N / 8000.0},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "gpu_launches_per_step": launches / args.steps,
             "clocks": clocks, "kernels": breakdown,
             "ms_per_step_instrumented": ms_prof,
         }
