@@ -59,7 +59,7 @@ def parse():
                     help="N > 1, modes p2p / zero: split the tensors into this many buckets (one plan "
                          "each) and run the step in two phases per bucket (fp8lm_dp_step_split), so "
                          "the exchange of one bucket overlaps the HBM passes of the others.  0 = auto: "
-                         "6 for sets above 1G params, else 1 (small sets are launch-bound)")
+                         "6 (p2p) or 4 (zero) for sets above 1G params, else 1 (small sets are launch-bound)")
     ap.add_argument("--bucket-lag", type=int, default=0,
                     help="split step issue order: 0 = phase 1 of every bucket then phase 2 of every "
                          "bucket; k = phase 2 of bucket b after phase 1 of bucket b + k")
@@ -422,7 +422,8 @@ def main():
     mode = ({"p2p": B.MODE_P2P, "nccl": B.MODE_NCCL, "zero": B.MODE_ZERO}[args.exchange]
             if N > 1 else (B.MODE_SIMULATED if sim else B.MODE_LOCAL))
     zero = mode == B.MODE_ZERO
-    nb = args.buckets if args.buckets > 0 else (6 if params > 1e9 else 1)
+    # auto: 6 buckets for P2P sets above 1G params, 4 for ZeRO (profiles/r2/split, zero_push)
+    nb = args.buckets if args.buckets > 0 else ((4 if args.exchange == "zero" else 6) if params > 1e9 else 1)
     if not (N > 1 and args.exchange in ("p2p", "zero")):
         nb = 1
     groups = B.bucket_split(numels, nb) if nb > 1 else [list(range(len(numels)))]
