@@ -136,6 +136,19 @@ def test_loopback_eight_ranks(B, variant):
                  specials=_huge, oneshot=_oneshot_arg(variant))
 
 
+@pytest.mark.parametrize("N", [2, 4])
+@pytest.mark.parametrize("numels", [[1500], [4096], [3, 64]], ids=["1500", "4096", "3+64"])
+@pytest.mark.parametrize("variant", ["fused", "unfused", "raw"])
+def test_loopback_oneshot_single_unit(B, N, numels, variant):
+    """Plans of one 4096-element unit launch the one-shot kernels as ONE CTA, which skips
+    the tickets and the phase word (k_oneshot, k_oneshot_full, k_oneshot_raw)."""
+    def spec(flat, r, step):                  # one saturating sum at step 2
+        if step == 2 and r == 1:
+            flat[1] = 3.0e5
+    run_loopback(B, numels, "p2p", N, steps=4, fused=variant != "unfused", specials=spec,
+                 oneshot="raw" if variant == "raw" else True)
+
+
 @pytest.mark.parametrize("N", [3, 4])
 @pytest.mark.parametrize("variant", ["p2p", "p2p_unfused", "p2p_delayed", "zero", "zero_unfused"])
 def test_loopback_tiny_shards(B, N, variant):
