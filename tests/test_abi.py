@@ -134,6 +134,27 @@ def test_plan_argument_errors(B):
     assert rc == B.EWORKSPACE
     B.lib.fp8lm_plan_destroy(h)
     assert B.lib.fp8lm_quantize(None, B.F32, -1, B.E4M3, None, None, None, None, 1, None, None) == B.EINVAL
+    # small-message thresholds: host setters, no GPU
+    rc, h = _plan(B, [1000, 24], B.MODE_P2P, 2, 0)
+    assert rc == 0
+    assert B.lib.fp8lm_plan_set_oneshot(h, 1 << 20) == 0
+    assert B.lib.fp8lm_plan_set_oneshot_raw(h, 0) == 0
+    assert B.lib.fp8lm_plan_set_oneshot_raw(h, -1) == B.EINVAL
+    assert B.lib.fp8lm_plan_set_oneshot(h, -1) == B.EINVAL
+    B.lib.fp8lm_plan_destroy(h)
+    assert B.lib.fp8lm_plan_set_oneshot_raw(None, 1) == B.EINVAL
+    # ZeRO: every rank's owned layout is the Alg. 1 packing of its tensors
+    numels = [5000, 70001, 3, 16384, 999, 64]
+    owners = []
+    for r in range(3):
+        rc, h = _plan(B, numels, B.MODE_ZERO, 3, r)
+        assert rc == 0
+        owned = [t for t in range(len(numels)) if B.lib.fp8lm_plan_owned_offset(h, t) >= 0]
+        assert B.lib.fp8lm_plan_owned_count(h) == len(owned)
+        assert B.lib.fp8lm_plan_owned_total(h) == sum((numels[t] + 63) // 64 * 64 for t in owned)
+        owners += owned
+        B.lib.fp8lm_plan_destroy(h)
+    assert sorted(owners) == list(range(len(numels)))      # every tensor has exactly one owner
 
 
 def test_workspace_sizes(B):
